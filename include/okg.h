@@ -1,0 +1,180 @@
+/*
+ * okg.h -- C ABI of the B200-native Newton linear solver (libokg.so).
+ *
+ * Drop-in boundary for the reference's Newton-solve path
+ * (okflow, /root/reference/proj/include/okflow).  Plain C types only: host or
+ * device pointers plus sizes, int64 sizes, negative status codes.  No C++
+ * exception crosses this boundary; okg/okflow.hpp maps the codes back onto the
+ * reference's exception types (errors.hpp:9-28).
+ *
+ * Vector convention: an N-vector holds one value per mesh vertex in the
+ * reference's global vertex order (x slowest, mesh.hpp:40-44); a stacked
+ * 2N-vector is [u-block ; w-block] exactly as precond.hpp:257-298 lays it out.
+ *
+ * Threading: one okg_ctx per GPU/thread, not re-entrant; every call is
+ * synchronous on return (the context's stream is drained).
+ */
+#ifndef OKG_H
+#define OKG_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OKG_ABI_VERSION 1
+
+/* opaque solver context: mesh + operators + SchurContext + Krylov workspace */
+typedef struct okg_ctx okg_ctx;
+
+/* ---- status codes: errors.hpp:9-28 + std::invalid_argument -------------- */
+enum okg_status {
+  OKG_OK = 0,
+  OKG_EINVAL = -1,        /* std::invalid_argument                        */
+  OKG_ENUMERICAL = -2,    /* okflow::NumericalError                       */
+  OKG_ECONFIG = -3,       /* okflow::ConfigError                          */
+  OKG_EINCONSISTENT = -4, /* okflow::InconsistentState                    */
+  OKG_ECOARSEN = -5,      /* okflow::CannotCoarsen                        */
+  OKG_ECUDA = -6,         /* CUDA runtime failure (no reference analogue) */
+  OKG_ENOMEM = -7,        /* device allocation failure                    */
+  OKG_EOTHER = -9
+};
+
+/* ---- okflow::SolverConfig (params.hpp:14-54) + context knobs ---------------- */
+typedef struct okg_params {
+  int32_t dim;              /* 2 or 3                                   */
+  int32_t n;                /* cells per axis                            */
+  double eps, sigma, m, theta, dt;
+  double newton_tol;
+  int32_t newton_maxit;
+  double gmres_tol;
+  int32_t gmres_maxit;
+  int32_t gmres_restart;    /* 0 = full GMRES (krylov.hpp:63)            */
+  int32_t cheby_iters;
+  int32_t richardson_steps;
+  int32_t mg_cycles, mg_pre, mg_post;
+  double mg_omega;
+  int32_t min_coarse_size;
+  double shat_perturb;      /* make_schur_context(..., shat_perturb), precond.hpp:126 */
+  int64_t max_dofs;         /* SolverConfig::max_dofs (validate only)    */
+  int32_t device;           /* CUDA device ordinal                       */
+  int32_t use_graphs;       /* capture the Arnoldi operator in a CUDA graph (default 1) */
+} okg_params;
+
+/* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
+#define OKG_MAX_NEWTON 64
+typedef struct okg_step_stats {
+  int32_t step;
+  double t;
+  int32_t newton_iters;
+  int32_t gmres_iters[OKG_MAX_NEWTON]; /* one per Newton iteration       */
+  double residual_norm;                /* final stacked nonlinear residual */
+  double seconds;                      /* wall time of newton_solve       */
+  int32_t converged;
+  int64_t kernel_launches;             /* kernels (incl. graph nodes) launched */
+} okg_step_stats;
+
+/* ---- okflow::KrylovResult (krylov.hpp:21-28) --------------------------------- */
+typedef struct okg_krylov_stats {
+  int32_t iterations;
+  int32_t converged;
+  int32_t stagnated;
+  double final_residual;
+  int32_t n_residual_norms;
+  double residual_norms[512]; /* first 512 recorded norms                 */
+} okg_krylov_stats;
+
+/* ---- read-only facts about a context ------------------------------------------ */
+typedef struct okg_info {
+  int32_t dim, n;
+  int64_t num_vertices;       /* N; stacked vectors have 2N entries       */
+  int32_t levels;             /* multigrid levels, finest = 0             */
+  int64_t level_size[32];
+  int32_t level_n[32];
+  double c, sqrt_c, a_coeff, dt_theta, lambda_lo, lambda_hi, eps_sqrt_c;
+  int64_t device_bytes;       /* device memory held by the context        */
+  int32_t graph_nodes;        /* kernels in the captured Arnoldi graph    */
+} okg_info;
+
+/* operator kinds for okg_apply (same numbering as the oracle's) */
+enum okg_op {
+  OKG_OP_M = 0,              /* spmv(M)                         sparse.hpp:138         */
+  OKG_OP_K = 1,              /* spmv(K)                                                */
+  OKG_OP_A = 2,              /* spmv(a_mat), a_mat=(1+dt*theta*sigma)M  precond.hpp:154 */
+  OKG_OP_SHAT = 3,           /* level operator Shat_l            multigrid.hpp:55-66   */
+  OKG_OP_PROLONG = 4,        /* P_l : level l+1 -> level l       mesh.hpp:169          */
+  OKG_OP_RESTRICT = 5,       /* P_l^T : level l -> level l+1     sparse.hpp:159        */
+  OKG_OP_VCYCLE = 6,         /* v_cycle                          multigrid.hpp:124     */
+  OKG_OP_SHAT_INV = 7,       /* apply_shat_inv                   multigrid.hpp:133     */
+  OKG_OP_CHEB_M = 8,         /* apply_M_inv                      precond.hpp:185       */
+  OKG_OP_CHEB_A = 9,         /* apply_A_inv                      precond.hpp:191       */
+  OKG_OP_ME = 10,            /* spmv(Me) at the linearization    assembly.hpp:153      */
+  OKG_OP_C = 11,             /* apply_C                          precond.hpp:244       */
+  OKG_OP_SCHUR = 12,         /* apply_schur                      precond.hpp:210       */
+  OKG_OP_SCHUR_TILDE_INV = 13, /* apply_schur_tilde_inv          precond.hpp:199       */
+  OKG_OP_S_INV_APPROX = 14,  /* apply_S_inv_approx               precond.hpp:227       */
+  OKG_OP_BLOCK = 15,         /* apply_block  (2N -> 2N)          precond.hpp:257       */
+  OKG_OP_JACOBIAN = 16,      /* jacobian_operator (2N -> 2N)     precond.hpp:277       */
+  OKG_OP_NONLINEAR = 17,     /* assemble_nonlinear(mesh, x)      assembly.hpp:194      */
+  OKG_OP_COARSE_SOLVE = 18   /* coarsest-level direct solve      dense.hpp:197         */
+};
+
+/* SolverConfig defaults (params.hpp:29-46) */
+int okg_default_params(okg_params* p);
+/* SolverConfig::validate (params.hpp:68-116) -> OKG_ECONFIG with message */
+int okg_validate_params(const okg_params* p);
+/* thread-local message of the last failing call */
+int okg_last_error(char* buf, size_t len);
+
+/* build_mesh + assemble_operators + make_schur_context, on `p->device`
+ * (replaces mesh.hpp:87, assembly.hpp:140, precond.hpp:126-181) */
+int okg_create(const okg_params* p, okg_ctx** ctx);
+void okg_destroy(okg_ctx* ctx);
+int okg_get_info(okg_ctx* ctx, okg_info* info);
+
+/* build_mesh arrays, bit-exact (mesh.hpp:87-157); host memory.
+ * vertices: N*dim doubles; cells: (2n^2 | 6n^3)*(dim+1) int32 */
+int okg_mesh(int32_t dim, int32_t n, double* vertices, int32_t* cells);
+/* the builder-defined seeded IC of SURVEY.md 8(d) (host) */
+int okg_seeded_ic(int64_t nverts, uint64_t seed, double m, double* u);
+
+/* okflow::State at the old time level (host arrays of N doubles) */
+int okg_set_state(okg_ctx* ctx, const double* u, const double* w, double t, int32_t step);
+int okg_get_state(okg_ctx* ctx, double* u, double* w, double* t, int32_t* step);
+/* newton_solve (model.hpp:165-215) from the current state; on return the
+ * context's state is the new time level.  Non-convergence is reported in
+ * stats->converged, not as an error (model.hpp:159-164). */
+int okg_newton_step(okg_ctx* ctx, okg_step_stats* stats);
+/* same, through host buffers: H2D of (u_old, w_old), solve, D2H of (u, w) */
+int okg_newton_step_host(okg_ctx* ctx, const double* u_old, const double* w_old,
+                         double* u_new, double* w_new, okg_step_stats* stats);
+
+/* ---- per-operator entry points on DEVICE pointers (parity + composition) ---- */
+/* ctx.Me = assemble_coefficient_mass(mesh, u) (model.hpp:184-185); u on device */
+int okg_linearize(okg_ctx* ctx, const double* u_dev);
+int okg_clear_linearization(okg_ctx* ctx);
+int okg_apply(okg_ctx* ctx, int32_t kind, int32_t level, const double* x_dev,
+              double* y_dev);
+/* residual (model.hpp:121-148) on device arrays */
+int okg_residual(okg_ctx* ctx, const double* u_next, const double* w_next,
+                 const double* u_old, const double* w_old, double* r1,
+                 double* r2);
+/* gmres(jacobian_operator, block_preconditioner, b, ...) (krylov.hpp:44) */
+int okg_gmres(okg_ctx* ctx, const double* b_dev, double* x_dev, double rel_tol,
+              int32_t max_iter, int32_t restart, okg_krylov_stats* stats);
+/* estimate_jacobi_spectrum(M) (krylov.hpp:296-320), recomputed on device */
+int okg_jacobi_spectrum(okg_ctx* ctx, double* lo, double* hi);
+
+/* ---- device memory helpers (so a C/ctypes caller needs no CUDA headers) ---- */
+int okg_device_alloc(int32_t device, size_t bytes, void** ptr);
+int okg_device_free(void* ptr);
+int okg_memcpy_h2d(void* dst_dev, const void* src_host, size_t bytes);
+int okg_memcpy_d2h(void* dst_host, const void* src_dev, size_t bytes);
+int okg_device_synchronize(void);
+/* total kernels this library has launched in this process (graph nodes counted) */
+int64_t okg_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

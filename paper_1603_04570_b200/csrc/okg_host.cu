@@ -1,0 +1,1362 @@
+// okg_host.cu -- host orchestration of the B200 Newton linear solve and the
+// C ABI of include/okg.h.
+//
+// Mirrors the reference call structure (file:line under
+// /root/reference/proj/include/okflow):
+//   make_schur_context   precond.hpp:126-181  -> okg_create
+//   build_hierarchy      multigrid.hpp:43-86  -> build_levels (rediscretised
+//                        Shat_l = M_l + eps*sqrt(c) K_l, equal to the Galerkin
+//                        P^T Shat P of the reference for nested P1 spaces)
+//   mg_cycle / v_cycle / apply_shat_inv  multigrid.hpp:97-149
+//   apply_M_inv/A_inv, apply_schur_tilde_inv, apply_schur, apply_S_inv_approx,
+//   apply_C, apply_block, jacobian_operator   precond.hpp:185-298
+//   gmres                krylov.hpp:44-152
+//   residual, newton_solve  model.hpp:121-215
+// Everything runs on one CUDA stream; the Arnoldi operator (block
+// preconditioner + Jacobian, ~300 kernels) is captured once into a CUDA
+// graph and replayed per GMRES iteration.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/okg.h"
+#include "okg_kernels.cuh"
+#include "okg_tables.h"
+
+namespace okg {
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+struct Status {
+  int code;
+};
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e__ = (call);                                                          \
+    if (e__ != cudaSuccess)                                                            \
+      throw Status{fail(OKG_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e__),   \
+                        __FILE__, __LINE__)};                                          \
+  } while (0)
+
+#define THROW(code, ...) throw Status{fail(code, __VA_ARGS__)}
+
+struct HostOp {
+  double w[15];
+  double invd;
+  double* tab = nullptr;  // device [ncls][noff+1]
+  std::vector<double> htab;
+};
+
+template <int DIM>
+static Op<DIM> dev_op(const HostOp& h) {
+  Op<DIM> o;
+  for (int q = 0; q < Traits<DIM>::NOFF; ++q) o.w[q] = h.w[q];
+  o.invd = h.invd;
+  o.tab = h.tab;
+  return o;
+}
+
+struct Level {
+  Grid g;
+  HostOp shat;
+  double *b = nullptr, *x = nullptr, *ea = nullptr, *eb = nullptr, *res = nullptr;
+};
+
+}  // namespace okg
+
+using namespace okg;
+
+struct okg_ctx {
+  okg_params p;
+  int dim = 0, n = 0;
+  uint32_t N = 0;
+  size_t N2 = 0;
+  double h = 0, c = 0, sqrt_c = 0, a_coeff = 0, dt_theta = 0, shat_scale = 1, eps_sqrt_c = 0;
+  double lambda_lo = 0, lambda_hi = 0;
+  std::vector<double> cheb_c1, cheb_c2;
+  double cheb_inv_theta = 0;
+  Grid fine;
+  HostOp M, K, A;
+  std::vector<Level> lv;
+  int nc = 0;
+  double* Ainv = nullptr;
+  double b_int = 0;
+  double* b_tab = nullptr;
+  Nonlin nl;
+  // linearisation
+  double* coef = nullptr;
+  bool have_lin = false;
+  // Krylov
+  int vcap = 0;
+  double* V = nullptr;
+  double *gb = nullptr, *gx = nullptr, *gr = nullptr, *pin = nullptr, *pz = nullptr, *pw = nullptr,
+         *gt = nullptr;
+  // preconditioner scratch
+  double *cd0 = nullptr, *cd1 = nullptr, *cr = nullptr, *r2p = nullptr, *sy = nullptr, *st = nullptr,
+         *kv = nullptr, *zz = nullptr, *rr = nullptr, *z2 = nullptr, *shr = nullptr;
+  // state
+  double *u_old = nullptr, *w_old = nullptr, *u = nullptr, *w = nullptr;
+  double t = 0;
+  int step = 0;
+  // reductions
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  double* dred = nullptr;
+  double* hred = nullptr;  // pinned
+  int* dflag = nullptr;
+  size_t max_blocks = 0;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t g_arn = nullptr, g_prec = nullptr;
+  int arn_nodes = 0, prec_nodes = 0;
+  bool capturing = false;
+  int cap_count = 0;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+};
+
+namespace okg {
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+static double* dalloc(okg_ctx* c, size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(double));
+  if (e != cudaSuccess) THROW(OKG_ENOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(double), cudaGetErrorString(e));
+  CK(cudaMemsetAsync(p, 0, n * sizeof(double), c->stream));
+  c->allocs.push_back(p);
+  c->bytes += n * sizeof(double);
+  return static_cast<double*>(p);
+}
+
+static void note(okg_ctx* c) {
+  if (c->capturing) c->cap_count++;
+  else g_launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) THROW(OKG_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+}
+
+static unsigned nblk(size_t n) { return static_cast<unsigned>((n + BS - 1) / BS); }
+static unsigned vblk(size_t n) { return static_cast<unsigned>(std::min<size_t>((n + BS - 1) / BS, 148 * 8)); }
+
+static Reduce red(okg_ctx* c, int off) { return Reduce{c->partials, c->ticket, c->dred + off}; }
+// layout of dred
+enum { R_H = 0, R_C = 40, R_NRM = 80, R_RES = 90, R_JRES = 95, R_DOT = 100 };
+
+static void sync_read(okg_ctx* c, int off, int cnt) {
+  CK(cudaMemcpyAsync(c->hred + off, c->dred + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+static Grid make_grid(int dim, int n) {
+  Grid g;
+  g.n = n;
+  g.s = n + 1;
+  g.ps = dim == 2 ? (uint32_t)g.s : (uint32_t)g.s * (uint32_t)g.s;
+  g.N = dim == 2 ? g.ps * (uint32_t)g.s : g.ps * (uint32_t)g.s;
+  const int noff = dim == 2 ? 7 : 15;
+  for (int o = 0; o < 15; ++o) {
+    if (o >= noff) {
+      g.off[o] = 0;
+      continue;
+    }
+    if (dim == 2) g.off[o] = off_comp(2, o, 0) * g.s + off_comp(2, o, 1);
+    else g.off[o] = off_comp(3, o, 0) * (int)g.ps + off_comp(3, o, 1) * g.s + off_comp(3, o, 2);
+  }
+  return g;
+}
+
+// weights w(cls,o) = a * U1(cls,o) + b * U2(cls,o)  (a*U1 when U2 null)
+static HostOp make_op(okg_ctx* c, const UnitTables& ut, const std::vector<double>& U1, double a,
+                      const std::vector<double>* U2, double b, bool add_form) {
+  HostOp op;
+  const int ncls = ut.ncls, noff = ut.noff, center = noff / 2;
+  const int interior = ncls / 2;
+  op.htab.assign(static_cast<size_t>(ncls) * (noff + 1), 0.0);
+  for (int cl = 0; cl < ncls; ++cl) {
+    for (int o = 0; o < noff; ++o) {
+      const double u1 = U1[static_cast<size_t>(cl) * noff + o];
+      double v = u1 * a;
+      if (U2) {
+        const double u2 = (*U2)[static_cast<size_t>(cl) * noff + o];
+        // add(M, alpha, K) (sparse.hpp:183-196): M_ij + alpha*K_ij
+        v = add_form ? v + b * u2 : v;
+      }
+      op.htab[static_cast<size_t>(cl) * (noff + 1) + o] = v;
+    }
+    const double d = op.htab[static_cast<size_t>(cl) * (noff + 1) + center];
+    if (!(d > 0.0)) THROW(OKG_ENUMERICAL, "operator: non-positive diagonal entry");
+    op.htab[static_cast<size_t>(cl) * (noff + 1) + noff] = 1.0 / d;
+  }
+  for (int o = 0; o < 15; ++o) op.w[o] = o < noff ? op.htab[static_cast<size_t>(interior) * (noff + 1) + o] : 0.0;
+  op.invd = op.htab[static_cast<size_t>(interior) * (noff + 1) + noff];
+  op.tab = dalloc(c, op.htab.size());
+  CK(cudaMemcpyAsync(op.tab, op.htab.data(), op.htab.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return op;
+}
+
+static double ipow(double h, int k) {
+  double r = 1.0;
+  for (int i = 0; i < k; ++i) r *= h;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// kernel launch wrappers (DIM-templated)
+// ---------------------------------------------------------------------------
+template <int DIM>
+static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const double* x, const double* b,
+                     double* y, double* acc, double omega = 0.0) {
+  const Op<DIM> o = dev_op<DIM>(op);
+  switch (epi) {
+    case EPI_APPLY: k_op<DIM, EPI_APPLY><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega); break;
+    case EPI_RESID: k_op<DIM, EPI_RESID><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega); break;
+    case EPI_JACOBI: k_op<DIM, EPI_JACOBI><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega); break;
+    case EPI_JACOBI_SET:
+      k_op<DIM, EPI_JACOBI_SET><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega);
+      break;
+    case EPI_JACOBI_ACC:
+      k_op<DIM, EPI_JACOBI_ACC><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega);
+      break;
+    case EPI_SCALE_APPLY:
+      k_op<DIM, EPI_SCALE_APPLY><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega);
+      break;
+  }
+  note(c);
+}
+
+static void axpy(okg_ctx* c, double a, const double* x, double* y, size_t n) {
+  k_axpy<<<vblk(n), BS, 0, c->stream>>>(a, x, y, n);
+  note(c);
+}
+static void scale(okg_ctx* c, double s, const double* x, double* y, size_t n) {
+  k_scale<<<vblk(n), BS, 0, c->stream>>>(s, x, y, n);
+  note(c);
+}
+static void copy(okg_ctx* c, const double* x, double* y, size_t n) {
+  CK(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// ---- multigrid (multigrid.hpp:97-149) --------------------------------------
+template <int DIM>
+static void coarse_solve(okg_ctx* c, const double* b, double* y) {
+  k_coarse_solve<<<(c->nc + BS / 32 - 1) / (BS / 32), BS, 0, c->stream>>>(c->nc, c->Ainv, b, y);
+  note(c);
+}
+
+template <int DIM>
+static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
+  Level& L = c->lv[l];
+  const int last = static_cast<int>(c->lv.size()) - 1;
+  if (l == last) {
+    if (!acc) {
+      coarse_solve<DIM>(c, rhs, out);
+    } else {
+      coarse_solve<DIM>(c, rhs, L.ea);
+      axpy(c, 1.0, L.ea, out, L.g.N);
+    }
+    return;
+  }
+  const double om = c->p.mg_omega;
+  const Op<DIM> op = dev_op<DIM>(L.shat);
+  double* cur = L.ea;
+  double* oth = L.eb;
+  const int pre = c->p.mg_pre, post = c->p.mg_post;
+  if (pre == 0) {
+    CK(cudaMemsetAsync(cur, 0, L.g.N * sizeof(double), c->stream));
+  } else if (pre >= 2) {
+    k_pre2<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
+    note(c);
+    for (int s = 2; s < pre; ++s) {
+      op_apply<DIM>(c, L.g, L.shat, EPI_JACOBI, cur, rhs, oth, nullptr, om);
+      std::swap(cur, oth);
+    }
+  } else {
+    k_jacobi0<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
+    note(c);
+  }
+  op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
+  Level& C = c->lv[l + 1];
+  k_restrict<DIM><<<nblk(C.g.N), BS, 0, c->stream>>>(L.g, C.g, L.res, C.b);
+  note(c);
+  mg_level<DIM>(c, l + 1, C.b, C.x, false);
+  k_prolong_add<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, C.g, C.x, cur);
+  note(c);
+  for (int s = 0; s < post; ++s) {
+    if (s == post - 1) {
+      op_apply<DIM>(c, L.g, L.shat, acc ? EPI_JACOBI_ACC : EPI_JACOBI_SET, cur, rhs, nullptr, out, om);
+    } else {
+      op_apply<DIM>(c, L.g, L.shat, EPI_JACOBI, cur, rhs, oth, nullptr, om);
+      std::swap(cur, oth);
+    }
+  }
+  if (post == 0) {
+    if (acc) axpy(c, 1.0, cur, out, L.g.N);
+    else copy(c, cur, out, L.g.N);
+  }
+}
+
+// apply_shat_inv (multigrid.hpp:133-149): `cycles` V-cycles composed by Richardson
+template <int DIM>
+static void shat_inv(okg_ctx* c, const double* b, double* x, int cycles) {
+  for (int cyc = 0; cyc < cycles; ++cyc) {
+    const double* rhs = cyc == 0 ? b : c->shr;
+    mg_level<DIM>(c, 0, rhs, x, cyc > 0);
+    if (cyc + 1 == cycles) break;
+    op_apply<DIM>(c, c->lv[0].g, c->lv[0].shat, EPI_RESID, x, b, c->shr, nullptr);
+  }
+}
+
+// ---- Chebyshev (krylov.hpp:158-202) ---------------------------------------------
+template <int DIM>
+static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
+  const Grid& g = c->fine;
+  const Op<DIM> o = dev_op<DIM>(A);
+  const int k = c->p.cheby_iters;
+  double* dcur = c->cd0;
+  double* dnxt = c->cd1;
+  k_cheb_first<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, o, b, dcur, c->cheb_inv_theta);
+  note(c);
+  if (k == 1) {
+    copy(c, dcur, x, g.N);
+    return;
+  }
+  for (int j = 0; j + 1 < k; ++j) {
+    const int last = (j == k - 2);
+    k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
+                                                      c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last);
+    note(c);
+    std::swap(dcur, dnxt);
+  }
+}
+
+// ---- u-dependent blocks ---------------------------------------------------------
+template <int DIM, int MODE>
+static void capply(okg_ctx* c, const double* x, const double* v, const double* b, double* y, double s1,
+                   Reduce rd = Reduce{nullptr, nullptr, nullptr}) {
+  CArgs a;
+  a.x = x;
+  a.v = v;
+  a.b = b;
+  a.y = y;
+  a.coef = c->coef;
+  a.ldc = c->N;
+  a.n2 = c->N;
+  a.s1 = s1;
+  a.s2 = 0.0;
+  k_capply<DIM, MODE><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K),
+                                                        dev_op<DIM>(c->A), a, rd);
+  note(c);
+}
+
+// apply_schur_tilde_inv (precond.hpp:199-205)
+template <int DIM>
+static void schur_tilde_inv(okg_ctx* c, const double* b, double* x) {
+  shat_inv<DIM>(c, b, c->sy, c->p.mg_cycles);
+  op_apply<DIM>(c, c->fine, c->M, EPI_APPLY, c->sy, nullptr, c->st, nullptr);
+  shat_inv<DIM>(c, c->st, x, c->p.mg_cycles);
+}
+
+// apply_schur (precond.hpp:210-222); resid: y = b - S v
+template <int DIM>
+static void apply_schur(okg_ctx* c, const double* v, const double* b, double* y) {
+  op_apply<DIM>(c, c->fine, c->K, EPI_APPLY, v, nullptr, c->kv, nullptr);
+  cheb<DIM>(c, c->M, c->kv, c->zz);
+  if (b) capply<DIM, CM_SCHUR_RES>(c, c->zz, v, b, y, c->c);
+  else capply<DIM, CM_SCHUR>(c, c->zz, v, nullptr, y, c->c);
+}
+
+// apply_S_inv_approx (precond.hpp:227-241) = richardson (krylov.hpp:225-242)
+template <int DIM>
+static void s_inv_approx(okg_ctx* c, const double* b, double* x) {
+  const int k = c->p.richardson_steps;
+  schur_tilde_inv<DIM>(c, b, x);
+  for (int j = 1; j < k; ++j) {
+    apply_schur<DIM>(c, x, b, c->rr);
+    schur_tilde_inv<DIM>(c, c->rr, c->z2);
+    axpy(c, 1.0, c->z2, x, c->N);
+  }
+}
+
+// apply_block (precond.hpp:257-271)
+template <int DIM>
+static void apply_block(okg_ctx* c, const double* p, double* z) {
+  cheb<DIM>(c, c->A, p, z);
+  capply<DIM, CM_SUB>(c, z, nullptr, p + c->N, c->r2p, 0.0);
+  s_inv_approx<DIM>(c, c->r2p, z + c->N);
+}
+
+template <int DIM>
+static void jacobian(okg_ctx* c, const double* x, double* y) {
+  capply<DIM, CM_JAC>(c, x, x + c->N, nullptr, y, c->dt_theta);
+}
+
+static void check_lin(okg_ctx* c, const char* what) {
+  if (!c->have_lin) THROW(OKG_EINCONSISTENT, "%s: linearized double-well block is not set", what);
+}
+
+// ---- graphs ------------------------------------------------------------------------
+template <int DIM>
+static void capture_graphs(okg_ctx* c) {
+  cudaGraph_t g;
+  c->capturing = true;
+  c->cap_count = 0;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    apply_block<DIM>(c, c->pin, c->pz);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    throw;
+  }
+  CK(cudaStreamEndCapture(c->stream, &g));
+  c->prec_nodes = c->cap_count;
+  CK(cudaGraphInstantiate(&c->g_prec, g, 0));
+  CK(cudaGraphDestroy(g));
+  c->cap_count = 0;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    apply_block<DIM>(c, c->pin, c->pz);
+    jacobian<DIM>(c, c->pz, c->pw);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    throw;
+  }
+  CK(cudaStreamEndCapture(c->stream, &g));
+  c->arn_nodes = c->cap_count;
+  CK(cudaGraphInstantiate(&c->g_arn, g, 0));
+  CK(cudaGraphDestroy(g));
+  c->capturing = false;
+}
+
+// z = P^{-1} pin  (and w = J z when `with_jac`)
+template <int DIM>
+static void run_arnoldi_op(okg_ctx* c, bool with_jac) {
+  if (c->p.use_graphs) {
+    CK(cudaGraphLaunch(with_jac ? c->g_arn : c->g_prec, c->stream));
+    g_launches += with_jac ? c->arn_nodes : c->prec_nodes;
+  } else {
+    apply_block<DIM>(c, c->pin, c->pz);
+    if (with_jac) jacobian<DIM>(c, c->pz, c->pw);
+  }
+}
+
+// ---- residual (model.hpp:121-148) ---------------------------------------------------
+template <int DIM>
+static double residual(okg_ctx* c, const double* un, const double* wn, const double* uo, const double* wo,
+                       double* o1, double* o2, double sign, double* s1out = nullptr) {
+  ResArgs a;
+  a.un = un;
+  a.wn = wn;
+  a.uo = uo;
+  a.wo = wo;
+  a.out1 = o1;
+  a.out2 = o2;
+  a.sign = sign;
+  a.dt_theta = c->p.dt * c->p.theta;
+  a.dt_1mtheta = c->p.dt * (1.0 - c->p.theta);
+  a.sigma = c->p.sigma;
+  a.m = c->p.m;
+  a.eps2 = c->p.eps * c->p.eps;
+  a.b_int = c->b_int;
+  a.b_tab = c->b_tab;
+  k_residual<DIM><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K), c->nl, a,
+                                                   red(c, R_RES));
+  note(c);
+  sync_read(c, R_RES, 2);
+  const double na = std::sqrt(c->hred[R_RES]), nb = std::sqrt(c->hred[R_RES + 1]);
+  if (s1out) *s1out = c->hred[R_RES] + c->hred[R_RES + 1];
+  return std::sqrt(na * na + nb * nb);  // stacked_norm, model.hpp:152-155
+}
+
+template <int DIM>
+static void linearize(okg_ctx* c, const double* u) {
+  k_linearize<DIM><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->K), c->nl, c->p.eps * c->p.eps, u,
+                                                    c->coef, c->N);
+  note(c);
+  c->have_lin = true;
+}
+
+// ---- GMRES (krylov.hpp:44-152) ----------------------------------------------------------
+static void givens(double cs, double sn, double& a, double& b) {
+  const double t = cs * a + sn * b;
+  b = -sn * a + cs * b;
+  a = t;
+}
+
+template <int NVB>
+static void arnoldi_ortho(okg_ctx* c, int nv) {
+  const size_t n2 = c->N2;
+  k_arnoldi_dot<NVB><<<vblk(n2), BS, 0, c->stream>>>(nv, c->pw, c->V, n2, n2, red(c, R_H));
+  note(c);
+  // put ||w||^2 after the h values at a fixed slot
+  k_arnoldi_update<NVB, 0><<<vblk(n2), BS, 0, c->stream>>>(nv, c->pw, c->V, n2, n2, c->dred + R_H, c->gt,
+                                                           red(c, R_C));
+  note(c);
+  k_arnoldi_update<NVB, 1><<<vblk(n2), BS, 0, c->stream>>>(nv, c->gt, c->V, n2, n2, c->dred + R_C, c->pw,
+                                                           red(c, R_NRM));
+  note(c);
+}
+
+// generic (nv > 32): chunked classical Gram-Schmidt twice
+static void arnoldi_ortho_chunked(okg_ctx* c, int nv, std::vector<double>& hsum, double& ww) {
+  const size_t n2 = c->N2;
+  hsum.assign(nv, 0.0);
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<double> hh(nv, 0.0);
+    for (int q0 = 0; q0 < nv; q0 += 32) {
+      const int cnt = std::min(32, nv - q0);
+      k_arnoldi_dot<32><<<vblk(n2), BS, 0, c->stream>>>(cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2, red(c, R_H));
+      note(c);
+      sync_read(c, R_H, 33);
+      for (int q = 0; q < cnt; ++q) hh[q0 + q] = c->hred[R_H + q];
+      if (pass == 0 && q0 == 0) ww = c->hred[R_H + 32];
+    }
+    for (int q0 = 0; q0 < nv; q0 += 32) {
+      const int cnt = std::min(32, nv - q0);
+      CK(cudaMemcpyAsync(c->dred + R_C, hh.data() + q0, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      k_arnoldi_update<32, 1><<<vblk(n2), BS, 0, c->stream>>>(cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2,
+                                                             c->dred + R_C, c->gt, red(c, R_NRM));
+      note(c);
+      copy(c, c->gt, c->pw, n2);
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    for (int q = 0; q < nv; ++q) hsum[q] += hh[q];
+  }
+  sync_read(c, R_NRM, 1);
+}
+
+template <int DIM>
+static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max_iter, int restart,
+                 okg_krylov_stats* st, double norm_b_sq = -1.0) {
+  const size_t n2 = c->N2;
+  okg_krylov_stats local;
+  if (!st) st = &local;
+  std::memset(st, 0, sizeof *st);
+  auto push = [&](double v) {
+    if (st->n_residual_norms < 512) st->residual_norms[st->n_residual_norms] = v;
+    st->n_residual_norms++;
+  };
+  CK(cudaMemsetAsync(x, 0, n2 * sizeof(double), c->stream));
+  double nb2 = norm_b_sq;
+  if (nb2 < 0.0) {
+    k_dot<<<vblk(n2), BS, 0, c->stream>>>(b, b, n2, red(c, R_DOT));
+    note(c);
+    sync_read(c, R_DOT, 1);
+    nb2 = c->hred[R_DOT];
+  }
+  // require_finite(b) (krylov.hpp:52): any NaN/Inf entry makes the sum of squares non-finite
+  if (!std::isfinite(nb2)) THROW(OKG_EINVAL, "gmres rhs: vector contains NaN/Inf");
+  const double norm_b = std::sqrt(nb2);
+  push(norm_b);
+  if (norm_b == 0.0) {
+    st->converged = 1;
+    return OKG_OK;
+  }
+  const double target = rel_tol * norm_b;
+  const int cycle_len = restart > 0 ? std::min(restart, max_iter) : max_iter;
+  if (cycle_len + 1 > c->vcap) THROW(OKG_EINVAL, "gmres: basis capacity %d < %d", c->vcap, cycle_len + 1);
+  const double* r = b;  // residual of the current iterate (x = 0)
+  double beta = norm_b;
+  std::vector<std::vector<double>> H;
+  std::vector<double> cs, sn, g, hsum;
+  while (st->iterations < max_iter) {
+    // V0 = r / beta
+    k_scale<<<vblk(n2), BS, 0, c->stream>>>(1.0 / beta, r, c->V, n2);
+    note(c);
+    copy(c, c->V, c->pin, n2);
+    H.clear();
+    cs.clear();
+    sn.clear();
+    g.assign(1, beta);
+    int j = 0;
+    bool breakdown = false;
+    while (j < cycle_len && st->iterations < max_iter) {
+      run_arnoldi_op<DIM>(c, true);  // pz = P^-1 V_j ; pw = J pz
+      const int nv = j + 1;
+      std::vector<double> h(j + 2, 0.0);
+      double ww, arnoldi_norm;
+      if (nv <= 32) {
+        if (nv <= 4) arnoldi_ortho<4>(c, nv);
+        else if (nv <= 8) arnoldi_ortho<8>(c, nv);
+        else if (nv <= 16) arnoldi_ortho<16>(c, nv);
+        else arnoldi_ortho<32>(c, nv);
+        // V_{j+1} = w / ||w||  (speculative; unused on exit)
+        k_normalize<<<vblk(n2), BS, 0, c->stream>>>(c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
+                                                     n2);
+        note(c);
+        const int nvb = nv <= 4 ? 4 : nv <= 8 ? 8 : nv <= 16 ? 16 : 32;
+        // dred[R_H + nvb] holds ||w||^2 (slot NVB of the first reduction)
+        CK(cudaMemcpyAsync(c->hred, c->dred, (R_NRM + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        ww = c->hred[R_H + nvb];
+        for (int q = 0; q < nv; ++q) h[q] = c->hred[R_H + q] + c->hred[R_C + q];
+        arnoldi_norm = std::sqrt(c->hred[R_NRM]);
+      } else {
+        arnoldi_ortho_chunked(c, nv, hsum, ww);
+        for (int q = 0; q < nv; ++q) h[q] = hsum[q];
+        arnoldi_norm = std::sqrt(c->hred[R_NRM]);
+        k_normalize<<<vblk(n2), BS, 0, c->stream>>>(c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
+                                                     n2);
+        note(c);
+      }
+      const double w_scale = std::sqrt(ww);
+      h[j + 1] = arnoldi_norm;
+      for (int i = 0; i < j; ++i) givens(cs[i], sn[i], h[i], h[i + 1]);
+      const double denom = std::hypot(h[j], h[j + 1]);
+      if (denom == 0.0) {
+        breakdown = true;
+        break;
+      }
+      const double cg = h[j] / denom, sg = h[j + 1] / denom;
+      h[j] = denom;
+      cs.push_back(cg);
+      sn.push_back(sg);
+      g.push_back(0.0);
+      givens(cg, sg, g[j], g[j + 1]);
+      H.push_back(std::move(h));
+      ++st->iterations;
+      ++j;
+      const double est = std::abs(g[j]);
+      push(est);
+      if (est <= target) break;
+      if (arnoldi_norm <= 1e-13 * w_scale) {
+        breakdown = true;
+        break;
+      }
+    }
+    // H y = g, u = sum y_i V_i, x += P^-1 u   (krylov.hpp:124-133)
+    std::vector<double> y(j, 0.0);
+    for (int i = j - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int k = i + 1; k < j; ++k) s -= H[k][i] * y[k];
+      y[i] = H[i][i] != 0.0 ? s / H[i][i] : 0.0;
+    }
+    for (int q0 = 0; q0 < std::max(j, 1); q0 += 32) {
+      Coeffs32 yc;
+      const int cnt = std::min(32, j - q0);
+      for (int q = 0; q < 32; ++q) yc.c[q] = q < cnt ? y[q0 + q] : 0.0;
+      if (q0 == 0) {
+        k_combine<<<vblk(n2), BS, 0, c->stream>>>(std::max(cnt, 0), yc, c->V, n2, n2, c->pin);
+        note(c);
+      } else {
+        k_combine<<<vblk(n2), BS, 0, c->stream>>>(cnt, yc, c->V + (size_t)q0 * n2, n2, n2, c->gt);
+        note(c);
+        axpy(c, 1.0, c->gt, c->pin, n2);
+      }
+    }
+    run_arnoldi_op<DIM>(c, false);  // pz = P^-1 u
+    axpy(c, 1.0, c->pz, x, n2);
+    // r = b - J x, beta = ||r||   (krylov.hpp:135-138)
+    capply<DIM, CM_JAC_RES>(c, x, x + c->N, b, c->gr, c->dt_theta, red(c, R_JRES));
+    sync_read(c, R_JRES, 1);
+    beta = std::sqrt(c->hred[R_JRES]);
+    st->final_residual = beta;
+    r = c->gr;
+    if (beta <= target * (1.0 + 1e-9)) {
+      st->converged = 1;
+      return OKG_OK;
+    }
+    if (breakdown) {
+      st->stagnated = 1;
+      return OKG_OK;
+    }
+    if (restart <= 0) return OKG_OK;
+  }
+  return OKG_OK;
+}
+
+// ---- Lanczos bounds (krylov.hpp:248-320) ------------------------------------------------
+template <int DIM>
+static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
+  const uint32_t n = c->N;
+  const int steps = (int)std::min<uint32_t>(30u, n);
+  std::mt19937 rng(1234u);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  std::vector<double> hv(n);
+  for (auto& e : hv) e = dist(rng);
+  std::vector<double*> Vv;
+  auto dot = [&](const double* a, const double* b) {
+    k_dot<<<vblk(n), BS, 0, c->stream>>>(a, b, n, red(c, R_DOT));
+    note(c);
+    sync_read(c, R_DOT, 1);
+    return c->hred[R_DOT];
+  };
+  // basis in the Krylov buffer space (gb, gx, ... are free at setup): use V if large enough
+  std::vector<double*> own;
+  auto vec = [&]() {
+    double* p = nullptr;
+    CK(cudaMalloc(&p, n * sizeof(double)));
+    own.push_back(p);
+    return p;
+  };
+  double* v0 = vec();
+  CK(cudaMemcpyAsync(v0, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const double nv0 = std::sqrt(dot(v0, v0));
+  scale(c, 1.0 / nv0, v0, v0, n);
+  Vv.push_back(v0);
+  double* w = vec();
+  std::vector<double> alpha, beta;
+  for (int j = 0; j < steps; ++j) {
+    op_apply<DIM>(c, c->fine, c->M, EPI_SCALE_APPLY, Vv[j], nullptr, w, nullptr);
+    const double a = dot(w, Vv[j]);
+    alpha.push_back(a);
+    axpy(c, -a, Vv[j], w, n);
+    if (j > 0) axpy(c, -beta[j - 1], Vv[j - 1], w, n);
+    for (double* q : Vv) axpy(c, -dot(w, q), q, w, n);
+    const double nb = std::sqrt(dot(w, w));
+    if (nb <= 1e-13 * std::abs(a) + 1e-300) break;
+    if (j + 1 < steps) {
+      beta.push_back(nb);
+      double* nvp = vec();
+      scale(c, 1.0 / nb, w, nvp, n);
+      Vv.push_back(nvp);
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  for (double* p : own) cudaFree(p);
+  const int m = static_cast<int>(alpha.size());
+  std::vector<double> T(static_cast<size_t>(m) * m, 0.0), ev;
+  for (int i = 0; i < m; ++i) {
+    T[i * m + i] = alpha[i];
+    if (i + 1 < m) {
+      T[i * m + i + 1] = beta[i];
+      T[(i + 1) * m + i] = beta[i];
+    }
+  }
+  if (!symmetric_eigenvalues(T, m, ev)) THROW(OKG_ENUMERICAL, "symmetric eigensolver failed to converge");
+  if (ev.front() < 0.0)
+    THROW(OKG_ENUMERICAL, "estimate_jacobi_spectrum: negative Ritz value, matrix not positive definite");
+  lo = 0.9 * ev.front();
+  hi = 1.1 * ev.back();
+}
+
+// ---- setup (make_schur_context, precond.hpp:126-181) ---------------------------------------
+template <int DIM>
+static void build(okg_ctx* c) {
+  const okg_params& p = c->p;
+  const UnitTables ut = build_unit_tables(DIM);
+  const int n = p.n;
+  c->h = 1.0 / n;
+  const double hd = ipow(c->h, DIM), hk = ipow(c->h, DIM - 2);
+  c->fine = make_grid(DIM, n);
+  c->N = c->fine.N;
+  c->N2 = 2 * (size_t)c->N;
+  c->M = make_op(c, ut, ut.M, hd, nullptr, 0.0, false);
+  c->K = make_op(c, ut, ut.K, hk, nullptr, 0.0, false);
+  {
+    // a_mat = scale(M, a_coeff): (M_ij) * a   (precond.hpp:154, sparse.hpp:198-202)
+    std::vector<double> Mh(ut.M.size());
+    for (size_t i = 0; i < Mh.size(); ++i) Mh[i] = ut.M[i] * hd;
+    c->A = make_op(c, ut, Mh, c->a_coeff, nullptr, 0.0, false);
+  }
+  // load vector per class
+  {
+    std::vector<double> bt(ut.ncls);
+    for (int cl = 0; cl < ut.ncls; ++cl) bt[cl] = ut.load[cl] * hd;
+    c->b_int = bt[ut.ncls / 2];
+    c->b_tab = dalloc(c, bt.size());
+    CK(cudaMemcpyAsync(c->b_tab, bt.data(), bt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  // closed-form nonlinear constants
+  const double fact = DIM == 2 ? 2.0 : 6.0;
+  c->nl.vol = hd / fact;
+  c->nl.kS = DIM == 2 ? (2.0 * 2.0 / 720.0) : (6.0 * 2.0 / 5040.0);
+  c->nl.kM = DIM == 2 ? (2.0 / 24.0) : (6.0 / 120.0);
+  c->nl.kT = DIM == 2 ? (2.0 * 6.0 / 720.0) : (6.0 * 6.0 / 5040.0);
+  // multigrid levels (build_hierarchy, multigrid.hpp:55-86)
+  {
+    int ln = n;
+    for (;;) {
+      Level L;
+      L.g = make_grid(DIM, ln);
+      const double hl = 1.0 / ln;
+      const double hld = ipow(hl, DIM), hlk = ipow(hl, DIM - 2);
+      std::vector<double> Ml(ut.M.size()), Kl(ut.K.size());
+      for (size_t i = 0; i < Ml.size(); ++i) {
+        Ml[i] = ut.M[i] * hld;
+        Kl[i] = ut.K[i] * hlk;
+      }
+      L.shat = make_op(c, ut, Ml, 1.0, &Kl, c->eps_sqrt_c, true);
+      c->lv.push_back(L);
+      if (!((int64_t)L.g.N > p.min_coarse_size && ln % 2 == 0)) break;
+      ln /= 2;
+    }
+    const int64_t coarsest = c->lv.back().g.N;
+    if (coarsest > std::max<int64_t>(p.min_coarse_size, 2000))
+      THROW(OKG_ECONFIG,
+            "build_hierarchy: coarsest level too large for a direct solve; choose a grid with more factors of two");
+    for (size_t l = 0; l < c->lv.size(); ++l) {
+      Level& L = c->lv[l];
+      const size_t nl = L.g.N;
+      if (l > 0) {
+        L.b = dalloc(c, nl);
+        L.x = dalloc(c, nl);
+      }
+      L.ea = dalloc(c, nl);
+      L.eb = dalloc(c, nl);
+      L.res = dalloc(c, nl);
+    }
+    // coarsest: dense SPD inverse (replaces CholeskyFactor, multigrid.hpp:82-83)
+    Level& Lc = c->lv.back();
+    const int nc = (int)Lc.g.N;
+    std::vector<double> Ad(static_cast<size_t>(nc) * nc, 0.0), Ai;
+    const int NO = Traits<DIM>::NOFF;
+    for (int i = 0; i < nc; ++i) {
+      int gi[3] = {0, 0, 0};
+      if (DIM == 2) {
+        gi[0] = i / Lc.g.s;
+        gi[1] = i % Lc.g.s;
+      } else {
+        gi[0] = i / (int)Lc.g.ps;
+        gi[1] = (i / Lc.g.s) % Lc.g.s;
+        gi[2] = i % Lc.g.s;
+      }
+      int cls = 0;
+      for (int d = 0; d < DIM; ++d) cls = cls * 3 + (gi[d] == 0 ? 0 : (gi[d] == Lc.g.n ? 2 : 1));
+      for (int o = 0; o < NO; ++o) {
+        bool ok = true;
+        for (int d = 0; d < DIM; ++d) {
+          const int v = gi[d] + off_comp(DIM, o, d);
+          ok = ok && v >= 0 && v <= Lc.g.n;
+        }
+        if (!ok) continue;
+        const int j = i + Lc.g.off[o];
+        Ad[static_cast<size_t>(i) * nc + j] = Lc.shat.htab[static_cast<size_t>(cls) * (NO + 1) + o];
+      }
+    }
+    if (!dense_spd_inverse(Ad, nc, Ai)) THROW(OKG_ENUMERICAL, "Cholesky: matrix not positive definite");
+    c->nc = nc;
+    c->Ainv = dalloc(c, Ai.size());
+    CK(cudaMemcpyAsync(c->Ainv, Ai.data(), Ai.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
+  // buffers
+  const size_t N = c->N, N2 = c->N2;
+  c->max_blocks = std::max<size_t>(nblk(N), 148 * 8) + 1;
+  c->partials = dalloc(c, c->max_blocks * 40);
+  {
+    void* t = nullptr;
+    CK(cudaMalloc(&t, 64));
+    CK(cudaMemsetAsync(t, 0, 64, c->stream));
+    c->allocs.push_back(t);
+    c->ticket = static_cast<unsigned*>(t);
+    c->dflag = reinterpret_cast<int*>(static_cast<char*>(t) + 32);
+  }
+  c->dred = dalloc(c, 256);
+  CK(cudaMallocHost(&c->hred, 256 * sizeof(double)));
+  c->coef = dalloc(c, (size_t)(Traits<DIM>::NPOS + 1) * N);
+  const int cycle_len = p.gmres_restart > 0 ? std::min(p.gmres_restart, p.gmres_maxit) : p.gmres_maxit;
+  c->vcap = cycle_len + 1;
+  c->V = dalloc(c, (size_t)c->vcap * N2);
+  c->gb = dalloc(c, N2);
+  c->gx = dalloc(c, N2);
+  c->gr = dalloc(c, N2);
+  c->pin = dalloc(c, N2);
+  c->pz = dalloc(c, N2);
+  c->pw = dalloc(c, N2);
+  c->gt = dalloc(c, N2);
+  for (double** b : {&c->cd0, &c->cd1, &c->cr, &c->r2p, &c->sy, &c->st, &c->kv, &c->zz, &c->rr, &c->z2, &c->shr,
+                     &c->u_old, &c->w_old, &c->u, &c->w})
+    *b = dalloc(c, N);
+  // Chebyshev bounds and coefficients
+  jacobi_spectrum<DIM>(c, c->lambda_lo, c->lambda_hi);
+  {
+    const double lmin = c->lambda_lo, lmax = c->lambda_hi;
+    if (lmin <= 0.0) THROW(OKG_EINVAL, "chebyshev: lambda_min must be positive");
+    if (lmax < lmin) THROW(OKG_EINVAL, "chebyshev: bounds out of order");
+    const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+    c->cheb_inv_theta = 1.0 / theta;
+    c->cheb_c1.assign(std::max(p.cheby_iters, 1), 0.0);
+    c->cheb_c2.assign(std::max(p.cheby_iters, 1), 1.0 / theta);
+    if (delta > 1e-300) {
+      const double sigma1 = theta / delta;
+      double rho = 1.0 / sigma1;
+      for (int j = 0; j + 1 < p.cheby_iters; ++j) {
+        const double rho_next = 1.0 / (2.0 * sigma1 - rho);
+        c->cheb_c1[j] = rho_next * rho;
+        c->cheb_c2[j] = 2.0 * rho_next / delta;
+        rho = rho_next;
+      }
+    }
+  }
+  if (p.use_graphs) capture_graphs<DIM>(c);
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace okg
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+#define DISPATCH(c, fn, ...) ((c)->dim == 2 ? fn<2>(__VA_ARGS__) : fn<3>(__VA_ARGS__))
+
+template <class F>
+static int guard(okg_ctx* c, F&& f) {
+  try {
+    if (c) {
+      cudaError_t e = cudaSetDevice(c->p.device);
+      if (e != cudaSuccess) return fail(OKG_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    }
+    f();
+    return OKG_OK;
+  } catch (const Status& s) {
+    return s.code;
+  } catch (const std::bad_alloc&) {
+    return fail(OKG_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(OKG_EOTHER, "%s", e.what());
+  }
+}
+
+template <int DIM>
+static void newton_step_impl(okg_ctx* c, okg_step_stats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const long long l0 = g_launches.load();
+  okg_step_stats st;
+  std::memset(&st, 0, sizeof st);
+  const okg_params& p = c->p;
+  const size_t N = c->N;
+  copy(c, c->u_old, c->u, N);
+  copy(c, c->w_old, c->w, N);
+  double s2 = 0.0;
+  // residual(next, old) with next = old; gb = -[R1; R2]  (model.hpp:178, :187-190)
+  double rnorm = residual<DIM>(c, c->u, c->w, c->u_old, c->w_old, c->gb, c->gb + N, -1.0, &s2);
+  const double ref = std::max(1.0, rnorm);
+  bool done = rnorm <= p.newton_tol * ref;
+  while (!done && st.newton_iters < p.newton_maxit) {
+    linearize<DIM>(c, c->u);  // Me at next.u (model.hpp:184-185)
+    okg_krylov_stats ks;
+    gmres<DIM>(c, c->gb, c->gx, p.gmres_tol, p.gmres_maxit, p.gmres_restart, &ks, s2);
+    if (st.newton_iters < OKG_MAX_NEWTON) st.gmres_iters[st.newton_iters] = ks.iterations;
+    // require_finite(lin.x) (model.hpp:196)
+    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
+    k_check_finite<<<vblk(c->N2), BS, 0, c->stream>>>(c->gx, c->N2, c->dflag);
+    note(c);
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (flag) {
+      c->have_lin = false;
+      THROW(OKG_EINVAL, "newton update: vector contains NaN/Inf");
+    }
+    axpy(c, 1.0, c->gx, c->u, N);
+    axpy(c, 1.0, c->gx + N, c->w, N);
+    ++st.newton_iters;
+    rnorm = residual<DIM>(c, c->u, c->w, c->u_old, c->w_old, c->gb, c->gb + N, -1.0, &s2);
+    done = rnorm <= p.newton_tol * ref;
+  }
+  c->have_lin = false;  // ctx.Me = nullptr (model.hpp:207)
+  CK(cudaStreamSynchronize(c->stream));
+  std::swap(c->u, c->u_old);
+  std::swap(c->w, c->w_old);
+  c->t += p.dt;
+  c->step += 1;
+  st.step = c->step;
+  st.t = c->t;
+  st.residual_norm = rnorm;
+  st.converged = done ? 1 : 0;
+  st.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  st.kernel_launches = g_launches.load() - l0;
+  if (stats) *stats = st;
+}
+
+template <int DIM>
+static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double* y) {
+  const int nlev = static_cast<int>(c->lv.size());
+  switch (kind) {
+    case OKG_OP_M: op_apply<DIM>(c, c->fine, c->M, EPI_APPLY, x, nullptr, y, nullptr); break;
+    case OKG_OP_K: op_apply<DIM>(c, c->fine, c->K, EPI_APPLY, x, nullptr, y, nullptr); break;
+    case OKG_OP_A: op_apply<DIM>(c, c->fine, c->A, EPI_APPLY, x, nullptr, y, nullptr); break;
+    case OKG_OP_SHAT:
+      if (level < 0 || level >= nlev) THROW(OKG_EINVAL, "level out of range");
+      op_apply<DIM>(c, c->lv[level].g, c->lv[level].shat, EPI_APPLY, x, nullptr, y, nullptr);
+      break;
+    case OKG_OP_PROLONG:
+      if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
+      CK(cudaMemsetAsync(y, 0, c->lv[level].g.N * sizeof(double), c->stream));
+      k_prolong_add<DIM><<<nblk(c->lv[level].g.N), BS, 0, c->stream>>>(c->lv[level].g, c->lv[level + 1].g, x, y);
+      note(c);
+      break;
+    case OKG_OP_RESTRICT:
+      if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
+      k_restrict<DIM><<<nblk(c->lv[level + 1].g.N), BS, 0, c->stream>>>(c->lv[level].g, c->lv[level + 1].g, x, y);
+      note(c);
+      break;
+    case OKG_OP_VCYCLE: mg_level<DIM>(c, 0, x, y, false); break;
+    case OKG_OP_SHAT_INV: shat_inv<DIM>(c, x, y, c->p.mg_cycles); break;
+    case OKG_OP_CHEB_M: cheb<DIM>(c, c->M, x, y); break;
+    case OKG_OP_CHEB_A: cheb<DIM>(c, c->A, x, y); break;
+    case OKG_OP_ME:
+      check_lin(c, "Me apply");
+      capply<DIM, CM_ME>(c, x, nullptr, nullptr, y, c->p.eps * c->p.eps);
+      break;
+    case OKG_OP_C:
+      check_lin(c, "constraint block");
+      capply<DIM, CM_C>(c, x, nullptr, nullptr, y, 0.0);
+      break;
+    case OKG_OP_SCHUR:
+      check_lin(c, "schur action");
+      apply_schur<DIM>(c, x, nullptr, y);
+      break;
+    case OKG_OP_SCHUR_TILDE_INV: schur_tilde_inv<DIM>(c, x, y); break;
+    case OKG_OP_S_INV_APPROX:
+      check_lin(c, "schur action");
+      s_inv_approx<DIM>(c, x, y);
+      break;
+    case OKG_OP_BLOCK:
+      check_lin(c, "block preconditioner");
+      apply_block<DIM>(c, x, y);
+      break;
+    case OKG_OP_JACOBIAN:
+      check_lin(c, "jacobian apply");
+      jacobian<DIM>(c, x, y);
+      break;
+    case OKG_OP_NONLINEAR:
+      k_nonlinear<DIM><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, c->nl, x, y);
+      note(c);
+      break;
+    case OKG_OP_COARSE_SOLVE: coarse_solve<DIM>(c, x, y); break;
+    default: THROW(OKG_EINVAL, "okg_apply: unknown kind %d", kind);
+  }
+}
+
+extern "C" {
+
+int okg_default_params(okg_params* p) {
+  if (!p) return fail(OKG_EINVAL, "null params");
+  std::memset(p, 0, sizeof *p);
+  p->dim = 2;
+  p->n = 64;
+  p->eps = 0.02;
+  p->sigma = 100.0;
+  p->m = 0.4;
+  p->theta = 0.5;
+  p->dt = 4.0e-4;
+  p->newton_tol = 1e-8;
+  p->newton_maxit = 20;
+  p->gmres_tol = 1e-6;
+  p->gmres_maxit = 200;
+  p->gmres_restart = 0;
+  p->cheby_iters = 10;
+  p->richardson_steps = 2;
+  p->mg_cycles = 5;
+  p->mg_pre = 2;
+  p->mg_post = 2;
+  p->mg_omega = 2.0 / 3.0;
+  p->min_coarse_size = 500;
+  p->shat_perturb = 0.0;
+  p->max_dofs = 2000000;
+  p->device = 0;
+  p->use_graphs = 1;
+  return OKG_OK;
+}
+
+int okg_validate_params(const okg_params* p) {
+  // SolverConfig::validate (params.hpp:68-116), fields present in okg_params
+  if (!(p->eps > 0.0)) return fail(OKG_ECONFIG, "config: eps must be positive");
+  if (p->sigma < 0.0) return fail(OKG_ECONFIG, "config: sigma must be nonnegative");
+  if (!(std::abs(p->m) < 1.0)) return fail(OKG_ECONFIG, "config: mean m must satisfy |m| < 1");
+  if (!(p->theta > 0.0) || p->theta > 1.0) return fail(OKG_ECONFIG, "config: theta must lie in (0, 1]");
+  if (!(p->dt > 0.0)) return fail(OKG_ECONFIG, "config: dt must be positive");
+  if (p->dim != 2 && p->dim != 3) return fail(OKG_ECONFIG, "config: dim must be 2 or 3");
+  if (p->n < 1) return fail(OKG_ECONFIG, "config: n must be at least 1");
+  if (!(p->newton_tol > 0.0)) return fail(OKG_ECONFIG, "config: newton_tol must be positive");
+  if (p->newton_maxit < 1) return fail(OKG_ECONFIG, "config: newton_maxit must be at least 1");
+  if (!(p->gmres_tol > 0.0)) return fail(OKG_ECONFIG, "config: gmres_tol must be positive");
+  if (p->gmres_maxit < 1) return fail(OKG_ECONFIG, "config: gmres_maxit must be at least 1");
+  if (p->gmres_restart < 0) return fail(OKG_ECONFIG, "config: gmres_restart must be nonnegative");
+  if (p->cheby_iters < 1) return fail(OKG_ECONFIG, "config: cheby_iters must be at least 1");
+  if (p->richardson_steps < 1) return fail(OKG_ECONFIG, "config: richardson_steps must be at least 1");
+  if (p->mg_cycles < 1) return fail(OKG_ECONFIG, "config: mg_cycles must be at least 1");
+  if (p->mg_pre < 0 || p->mg_post < 0 || p->mg_pre + p->mg_post < 1)
+    return fail(OKG_ECONFIG, "config: need at least one smoothing sweep per cycle");
+  if (!(p->mg_omega > 0.0) || !(p->mg_omega < 2.0)) return fail(OKG_ECONFIG, "config: mg_omega must lie in (0, 2)");
+  if (p->min_coarse_size < 1) return fail(OKG_ECONFIG, "config: min_coarse_size must be at least 1");
+  if (p->max_dofs < 1) return fail(OKG_ECONFIG, "config: max_dofs must be at least 1");
+  int64_t s = (int64_t)p->n + 1, v = s * s;
+  if (p->dim == 3) v *= s;
+  if (v > p->max_dofs)
+    return fail(OKG_ECONFIG, "config: mesh has %lld vertices, exceeding max_dofs = %lld", (long long)v,
+                (long long)p->max_dofs);
+  return OKG_OK;
+}
+
+int okg_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::strncpy(buf, g_err.c_str(), len - 1);
+    buf[len - 1] = 0;
+  }
+  return static_cast<int>(g_err.size());
+}
+
+static void destroy_ctx(okg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->p.device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->g_arn) cudaGraphExecDestroy(c->g_arn);
+  if (c->g_prec) cudaGraphExecDestroy(c->g_prec);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->hred) cudaFreeHost(c->hred);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int okg_create(const okg_params* p, okg_ctx** out) {
+  if (!p || !out) return fail(OKG_EINVAL, "okg_create: null argument");
+  *out = nullptr;
+  okg_ctx* c = new okg_ctx();
+  c->p = *p;
+  const int st = guard(nullptr, [&] {
+    // argument checks of build_mesh (mesh.hpp:88-90), make_schur_context (precond.hpp:132-147),
+    // compute_c (precond.hpp:31-38)
+    if (p->dim != 2 && p->dim != 3) THROW(OKG_EINVAL, "build_mesh: dim must be 2 or 3");
+    if (p->n < 1) THROW(OKG_EINVAL, "build_mesh: n must be positive");
+    if (!(p->eps > 0.0)) THROW(OKG_EINVAL, "schur context: eps must be positive");
+    const double scale_factor = 1.0 + p->shat_perturb;
+    if (!(scale_factor > 0.0))
+      THROW(OKG_EINVAL, "schur context: perturbation must keep the shifted operator positive");
+    if (!(p->dt > 0.0)) THROW(OKG_EINVAL, "compute_c: dt must be positive");
+    if (!(p->theta > 0.0) || p->theta > 1.0) THROW(OKG_EINVAL, "compute_c: theta must lie in (0, 1]");
+    if (p->sigma < 0.0) THROW(OKG_EINVAL, "compute_c: sigma must be nonnegative");
+    if (p->min_coarse_size < 1) THROW(OKG_EINVAL, "build_hierarchy: min_coarse_size < 1");
+    if (p->cheby_iters < 1) THROW(OKG_EINVAL, "chebyshev: need at least one step");
+    if (p->richardson_steps < 1) THROW(OKG_EINVAL, "schur solve: need at least one refinement step");
+    if (p->mg_cycles < 1 || p->mg_pre < 0 || p->mg_post < 0) THROW(OKG_EINVAL, "multigrid: bad cycle settings");
+    if (p->gmres_maxit < 1 || p->gmres_restart < 0) THROW(OKG_EINVAL, "gmres: bad iteration settings");
+    const int64_t s = (int64_t)p->n + 1;
+    const int64_t nv = p->dim == 2 ? s * s : s * s * s;
+    if (nv >= (int64_t)1 << 31) THROW(OKG_EINVAL, "mesh too large for one device (%lld vertices)", (long long)nv);
+    c->dim = p->dim;
+    c->n = p->n;
+    c->c = p->dt * p->theta / (1.0 + p->dt * p->theta * p->sigma);
+    c->sqrt_c = std::sqrt(c->c);
+    c->a_coeff = 1.0 + p->dt * p->theta * p->sigma;
+    c->dt_theta = p->dt * p->theta;
+    c->shat_scale = scale_factor;
+    c->eps_sqrt_c = c->shat_scale * p->eps * c->sqrt_c;
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (c->dim == 2) build<2>(c);
+    else build<3>(c);
+  });
+  if (st != OKG_OK) {
+    destroy_ctx(c);
+    return st;
+  }
+  *out = c;
+  return OKG_OK;
+}
+
+void okg_destroy(okg_ctx* c) { destroy_ctx(c); }
+
+int okg_get_info(okg_ctx* c, okg_info* info) {
+  if (!c || !info) return fail(OKG_EINVAL, "null argument");
+  std::memset(info, 0, sizeof *info);
+  info->dim = c->dim;
+  info->n = c->n;
+  info->num_vertices = c->N;
+  info->levels = static_cast<int>(c->lv.size());
+  for (size_t l = 0; l < c->lv.size() && l < 32; ++l) {
+    info->level_size[l] = c->lv[l].g.N;
+    info->level_n[l] = c->lv[l].g.n;
+  }
+  info->c = c->c;
+  info->sqrt_c = c->sqrt_c;
+  info->a_coeff = c->a_coeff;
+  info->dt_theta = c->dt_theta;
+  info->lambda_lo = c->lambda_lo;
+  info->lambda_hi = c->lambda_hi;
+  info->eps_sqrt_c = c->eps_sqrt_c;
+  info->device_bytes = static_cast<int64_t>(c->bytes);
+  info->graph_nodes = c->arn_nodes;
+  return OKG_OK;
+}
+
+int okg_mesh(int32_t dim, int32_t n, double* vertices, int32_t* cells) {
+  // build_mesh (mesh.hpp:87-157): same vertex order and cell connectivity
+  if (dim != 2 && dim != 3) return fail(OKG_EINVAL, "build_mesh: dim must be 2 or 3");
+  if (n < 1) return fail(OKG_EINVAL, "build_mesh: n must be positive");
+  const double h = 1.0 / n;
+  const int s = n + 1;
+  auto gi = [&](int i, int j, int k) { return dim == 2 ? i * s + j : (i * s + j) * s + k; };
+  size_t p = 0, q = 0;
+  if (dim == 2) {
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < s; ++j) {
+        vertices[p++] = i * h;
+        vertices[p++] = j * h;
+      }
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        const int a = gi(i, j, 0), b = gi(i + 1, j, 0), cc = gi(i + 1, j + 1, 0), d = gi(i, j + 1, 0);
+        const int v[6] = {a, b, cc, a, cc, d};
+        for (int t = 0; t < 6; ++t) cells[q++] = v[t];
+      }
+  } else {
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < s; ++j)
+        for (int k = 0; k < s; ++k) {
+          vertices[p++] = i * h;
+          vertices[p++] = j * h;
+          vertices[p++] = k * h;
+        }
+    static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    static const bool odd[6] = {false, true, true, false, false, true};
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        for (int k = 0; k < n; ++k)
+          for (int pp = 0; pp < 6; ++pp) {
+            int g[3] = {i, j, k};
+            int idx[4];
+            idx[0] = gi(g[0], g[1], g[2]);
+            for (int v = 1; v < 4; ++v) {
+              g[perms[pp][v - 1]] += 1;
+              idx[v] = gi(g[0], g[1], g[2]);
+            }
+            if (odd[pp]) std::swap(idx[1], idx[2]);
+            for (int t = 0; t < 4; ++t) cells[q++] = idx[t];
+          }
+  }
+  return OKG_OK;
+}
+
+int okg_seeded_ic(int64_t nverts, uint64_t seed, double m, double* u) {
+  // counter-based splitmix64 keyed by (seed, global vertex id)
+  for (int64_t g = 0; g < nverts; ++g) {
+    uint64_t x = seed * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(g) + 0x632BE59BD9B4E019ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x = x ^ (x >> 31);
+    const double U = 2.0 * (static_cast<double>(x >> 11) * 0x1.0p-53) - 1.0;
+    u[g] = m + 0.01 * U;
+  }
+  return OKG_OK;
+}
+
+int okg_set_state(okg_ctx* c, const double* u, const double* w, double t, int32_t step) {
+  if (!c || !u || !w) return fail(OKG_EINVAL, "okg_set_state: null argument");
+  return guard(c, [&] {
+    CK(cudaMemcpyAsync(c->u_old, u, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_old, w, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->t = t;
+    c->step = step;
+  });
+}
+
+int okg_get_state(okg_ctx* c, double* u, double* w, double* t, int32_t* step) {
+  if (!c) return fail(OKG_EINVAL, "okg_get_state: null context");
+  return guard(c, [&] {
+    if (u) CK(cudaMemcpyAsync(u, c->u_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (w) CK(cudaMemcpyAsync(w, c->w_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (t) *t = c->t;
+    if (step) *step = c->step;
+  });
+}
+
+int okg_newton_step(okg_ctx* c, okg_step_stats* stats) {
+  if (!c) return fail(OKG_EINVAL, "okg_newton_step: null context");
+  return guard(c, [&] { DISPATCH(c, newton_step_impl, c, stats); });
+}
+
+int okg_newton_step_host(okg_ctx* c, const double* u_old, const double* w_old, double* u_new, double* w_new,
+                         okg_step_stats* stats) {
+  if (!c || !u_old || !w_old || !u_new || !w_new) return fail(OKG_EINVAL, "okg_newton_step_host: null argument");
+  return guard(c, [&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    CK(cudaMemcpyAsync(c->u_old, u_old, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->w_old, w_old, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    DISPATCH(c, newton_step_impl, c, stats);
+    CK(cudaMemcpyAsync(u_new, c->u_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(w_new, c->w_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int okg_linearize(okg_ctx* c, const double* u_dev) {
+  if (!c || !u_dev) return fail(OKG_EINVAL, "okg_linearize: null argument");
+  return guard(c, [&] {
+    DISPATCH(c, linearize, c, u_dev);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int okg_clear_linearization(okg_ctx* c) {
+  if (!c) return fail(OKG_EINVAL, "null context");
+  c->have_lin = false;
+  return OKG_OK;
+}
+
+int okg_apply(okg_ctx* c, int32_t kind, int32_t level, const double* x, double* y) {
+  if (!c || !x || !y) return fail(OKG_EINVAL, "okg_apply: null argument");
+  return guard(c, [&] {
+    DISPATCH(c, apply_impl, c, kind, level, x, y);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int okg_residual(okg_ctx* c, const double* un, const double* wn, const double* uo, const double* wo, double* r1,
+                 double* r2) {
+  if (!c || !un || !wn || !uo || !wo || !r1 || !r2) return fail(OKG_EINVAL, "okg_residual: null argument");
+  return guard(c, [&] { DISPATCH(c, residual, c, un, wn, uo, wo, r1, r2, 1.0, nullptr); });
+}
+
+int okg_gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t restart,
+              okg_krylov_stats* stats) {
+  if (!c || !b || !x) return fail(OKG_EINVAL, "okg_gmres: null argument");
+  return guard(c, [&] {
+    check_lin(c, "jacobian apply");
+    DISPATCH(c, gmres, c, b, x, rel_tol, max_iter, restart, stats, -1.0);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int okg_jacobi_spectrum(okg_ctx* c, double* lo, double* hi) {
+  if (!c || !lo || !hi) return fail(OKG_EINVAL, "null argument");
+  return guard(c, [&] { DISPATCH(c, jacobi_spectrum, c, *lo, *hi); });
+}
+
+int okg_device_alloc(int32_t device, size_t bytes, void** ptr) {
+  return guard(nullptr, [&] {
+    CK(cudaSetDevice(device));
+    CK(cudaMalloc(ptr, bytes));
+  });
+}
+int okg_device_free(void* ptr) {
+  return guard(nullptr, [&] { CK(cudaFree(ptr)); });
+}
+int okg_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  return guard(nullptr, [&] { CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+int okg_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  return guard(nullptr, [&] { CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost)); });
+}
+int okg_device_synchronize(void) {
+  return guard(nullptr, [&] { CK(cudaDeviceSynchronize()); });
+}
+int64_t okg_kernel_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"
