@@ -165,6 +165,25 @@ int okg_gmres(okg_ctx* ctx, const double* b_dev, double* x_dev, double rel_tol,
 /* estimate_jacobi_spectrum(M) (krylov.hpp:296-320), recomputed on device */
 int okg_jacobi_spectrum(okg_ctx* ctx, double* lo, double* hi);
 
+/* ---- measurement hooks (bench.py) ---------------------------------------- */
+/* the context's CUDA stream (cudaStream_t) -- for events around a region */
+int okg_stream(okg_ctx* ctx, void** stream);
+/* fine-level kernels timed live with CUDA events on the context stream:
+ * `which` = OKG_KT_* ; avg_ms = mean launch duration over `reps` launches on
+ * the context's buffers ; bytes = algorithmic bytes one launch must move */
+enum okg_kernel_id {
+  OKG_KT_SMOOTH = 0,     /* damped-Jacobi sweep on Shat_0  (x, b -> y)          */
+  OKG_KT_RESID = 1,      /* residual b - Shat_0 x                               */
+  OKG_KT_PRE2 = 2,       /* fused two pre-smoothing sweeps from zero (r -> e)   */
+  OKG_KT_POST_ACC = 3,   /* last post-smooth fused with x += e                  */
+  OKG_KT_CHEB = 4,       /* one Chebyshev step (d, r, x -> d', r', x')          */
+  OKG_KT_JACOBIAN = 5,   /* fused block Jacobian apply                          */
+  OKG_KT_RESTRICT = 6,   /* P^T on the finest level                             */
+  OKG_KT_PROLONG = 7,    /* x += P e_c on the finest level                      */
+  OKG_KT_COUNT = 8
+};
+int okg_kernel_timing(okg_ctx* ctx, int32_t which, int32_t reps, double* avg_ms, double* bytes);
+
 /* ---- device memory helpers (so a C/ctypes caller needs no CUDA headers) ---- */
 int okg_device_alloc(int32_t device, size_t bytes, void** ptr);
 int okg_device_free(void* ptr);

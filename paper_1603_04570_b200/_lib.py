@@ -28,6 +28,8 @@ OP_S_INV_APPROX, OP_BLOCK, OP_JACOBIAN, OP_NONLINEAR, OP_COARSE_SOLVE = range(14
 
 OKG_MAX_NEWTON = 64
 
+KT_NAMES = ["smooth", "resid", "pre2", "post_acc", "cheb", "jacobian", "restrict", "prolong"]
+
 
 class Params(C.Structure):
     _fields_ = [
@@ -135,6 +137,8 @@ _SIGS = {
     "okg_residual": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "okg_gmres": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, C.POINTER(KrylovStats)]),
     "okg_jacobi_spectrum": (C.c_int, [_vp, _dp, _dp]),
+    "okg_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "okg_kernel_timing": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
     "okg_device_alloc": (C.c_int, [C.c_int32, C.c_size_t, C.POINTER(_vp)]),
     "okg_device_free": (C.c_int, [_vp]),
     "okg_memcpy_h2d": (C.c_int, [_vp, _vp, C.c_size_t]),

@@ -1339,6 +1339,86 @@ int okg_jacobi_spectrum(okg_ctx* c, double* lo, double* hi) {
   return guard(c, [&] { DISPATCH(c, jacobi_spectrum, c, *lo, *hi); });
 }
 
+int okg_stream(okg_ctx* c, void** stream) {
+  if (!c || !stream) return fail(OKG_EINVAL, "null argument");
+  *stream = reinterpret_cast<void*>(c->stream);
+  return OKG_OK;
+}
+
+}  // extern "C"
+
+template <int DIM>
+static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, double* bytes) {
+  Level& L0 = c->lv[0];
+  const Grid& g = L0.g;
+  const double om = c->p.mg_omega;
+  const double N = (double)g.N;
+  const double B = 8.0;
+  // operands: reuse workspace vectors (contents are finite)
+  double *x = c->cd0, *b = c->cd1, *y = c->cr, *z = c->kv;
+  auto launch = [&]() {
+    switch (which) {
+      case OKG_KT_SMOOTH: op_apply<DIM>(c, g, L0.shat, EPI_JACOBI, x, b, y, nullptr, om); break;
+      case OKG_KT_RESID: op_apply<DIM>(c, g, L0.shat, EPI_RESID, x, b, y, nullptr); break;
+      case OKG_KT_PRE2:
+        k_pre2<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(L0.shat), b, y, om);
+        note(c);
+        break;
+      case OKG_KT_POST_ACC: op_apply<DIM>(c, g, L0.shat, EPI_JACOBI_ACC, x, b, nullptr, z, om); break;
+      case OKG_KT_CHEB:
+        k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(c->A), x, b, y, z, c->zz, c->rr,
+                                                          c->cheb_c1[0], c->cheb_c2[0], 0);
+        note(c);
+        break;
+      case OKG_KT_JACOBIAN: jacobian<DIM>(c, c->pz, c->pw); break;
+      case OKG_KT_RESTRICT:
+        k_restrict<DIM><<<nblk(c->lv[1].g.N), BS, 0, c->stream>>>(g, c->lv[1].g, x, c->lv[1].b);
+        note(c);
+        break;
+      case OKG_KT_PROLONG:
+        k_prolong_add<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, c->lv[1].g, c->lv[1].x, y);
+        note(c);
+        break;
+      default: THROW(OKG_EINVAL, "okg_kernel_timing: unknown kernel %d", which);
+    }
+  };
+  if ((which == OKG_KT_RESTRICT || which == OKG_KT_PROLONG) && c->lv.size() < 2)
+    THROW(OKG_EINVAL, "okg_kernel_timing: single-level hierarchy");
+  const double Nc = c->lv.size() > 1 ? (double)c->lv[1].g.N : 0.0;
+  const double npos = Traits<DIM>::NPOS + 1;
+  switch (which) {
+    case OKG_KT_SMOOTH: case OKG_KT_RESID: *bytes = 3 * N * B; break;
+    case OKG_KT_PRE2: *bytes = 2 * N * B; break;
+    case OKG_KT_POST_ACC: *bytes = 4 * N * B; break;
+    case OKG_KT_CHEB: *bytes = 6 * N * B; break;
+    case OKG_KT_JACOBIAN: *bytes = (4 + npos) * N * B; break;
+    case OKG_KT_RESTRICT: *bytes = (N + Nc) * B; break;
+    case OKG_KT_PROLONG: *bytes = (2 * N + Nc) * B; break;
+  }
+  bool had_lin = c->have_lin;
+  for (int i = 0; i < 3; ++i) launch();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, c->stream));
+  for (int i = 0; i < reps; ++i) launch();
+  CK(cudaEventRecord(e1, c->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *avg_ms = (double)ms / reps;
+  c->have_lin = had_lin;
+}
+
+extern "C" {
+
+int okg_kernel_timing(okg_ctx* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {
+  if (!c || !avg_ms || !bytes || reps < 1) return fail(OKG_EINVAL, "okg_kernel_timing: bad argument");
+  return guard(c, [&] { DISPATCH(c, kernel_timing_impl, c, which, reps, avg_ms, bytes); });
+}
+
 int okg_device_alloc(int32_t device, size_t bytes, void** ptr) {
   return guard(nullptr, [&] {
     CK(cudaSetDevice(device));

@@ -25,6 +25,11 @@ CASES = [
     ("d2n16", 2, 16, 0.1, 0.02, 1),
     ("d3n4", 3, 4, 0.0, 0.02, 2),
     ("d3n8", 3, 8, 0.0, 0.02, 2),
+    # deep hierarchies down to n = 2 / n = 1 grids (min_coarse_size lowered)
+    ("d2n16mg", 2, 16, 0.0, 0.02, 3, 20),
+    ("d3n8mg", 3, 8, 0.0, 0.02, 4, 10),
+    # non-default eps / mean
+    ("d2n32e01", 2, 32, 0.1, 0.01, 1),
 ]
 
 OPS = [("M", po.M), ("K", po.K), ("A", po.A), ("VCYCLE", po.VCYCLE), ("SHAT_INV", po.SHAT_INV),
@@ -39,6 +44,7 @@ def make(name, dim, n, m, eps, seed, min_coarse=None):
     N = o.n
     rng = np.random.default_rng(1000 + dim * 100 + n)
     out = {"dim": dim, "n": n, "m": m, "eps": eps, "seed": seed, "N": N,
+           "min_coarse": p.min_coarse_size,
            "levels": np.array([o.level_size(l) for l in range(o.levels)])}
     sc = o.scalars()
     out["scalars"] = np.array([sc[k] for k in ("c", "sqrt_c", "a_coeff", "dt_theta", "lambda_lo",

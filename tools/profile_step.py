@@ -1,0 +1,24 @@
+"""Setup + exactly K Newton timesteps of a BASELINE workload, for ncu launch
+lists: prints the number of kernels launched during setup (pass it to ncu -s)
+and per step.  usage: python tools/profile_step.py DIM N [K] [seed]"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1603_04570_b200 as okg  # noqa: E402
+from paper_1603_04570_b200 import _lib  # noqa: E402
+
+dim, n = int(sys.argv[1]), int(sys.argv[2])
+k = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+seed = int(sys.argv[4]) if len(sys.argv) > 4 else (2 if dim == 3 else 0)
+cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30)
+ctx = okg.SchurContext(cfg)
+ctx.set_state(okg.State(okg.seeded_ic(ctx.n, seed, 0.0), np.zeros(ctx.n)))
+setup = _lib.lib.okg_kernel_launch_count()
+print(f"setup_launches={setup}", flush=True)
+for i in range(k):
+    st = ctx.step_resident()
+    print(f"step {i}: newton={st.newton_iters} gmres={st.gmres_iters} t={st.seconds*1e3:.2f}ms "
+          f"launches={st.kernel_launches}", flush=True)
