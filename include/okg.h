@@ -59,6 +59,8 @@ typedef struct okg_params {
   int64_t max_dofs;         /* SolverConfig::max_dofs (validate only)    */
   int32_t device;           /* CUDA device ordinal                       */
   int32_t use_graphs;       /* capture the Arnoldi operator in a CUDA graph (default 1) */
+  int32_t tiled_min_n;      /* levels with n >= this use the shared-memory tiled stencil
+                               kernels; 0 = default (3D: 32, 2D: 128), < 0 = never */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -179,7 +181,7 @@ enum okg_kernel_id {
   OKG_KT_CHEB = 4,       /* one Chebyshev step (d, r, x -> d', r', x')          */
   OKG_KT_JACOBIAN = 5,   /* fused block Jacobian apply                          */
   OKG_KT_RESTRICT = 6,   /* P^T on the finest level                             */
-  OKG_KT_PROLONG = 7,    /* x += P e_c on the finest level                      */
+  OKG_KT_PROLONG = 7,    /* x += P e_c (tiled levels: fused with the first post-smooth) */
   OKG_KT_COUNT = 8
 };
 int okg_kernel_timing(okg_ctx* ctx, int32_t which, int32_t reps, double* avg_ms, double* bytes);

@@ -69,7 +69,8 @@ class SolverConfig:
         s = self.n + 1
         return s ** self.dim
 
-    def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True) -> _lib.Params:
+    def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
+                  tiled_min_n: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -79,6 +80,7 @@ class SolverConfig:
         p.shat_perturb = shat_perturb
         p.device = device
         p.use_graphs = 1 if use_graphs else 0
+        p.tiled_min_n = tiled_min_n
         return p
 
     def validate(self) -> None:
@@ -226,13 +228,14 @@ class DeviceArray:
 # --------------------------------------------------------------------------------------
 class SchurContext:
     def __init__(self, cfg: SolverConfig, device: int = 0, shat_perturb: float = 0.0,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, tiled_min_n: int = 0):
         if cfg.cheby_precond != "jacobi":
             raise ConfigError("schur context: only cheby_precond = 'jacobi' is implemented on the GPU path")
         self.cfg = cfg
         self.device = device
         self.handle = C.c_void_p()
-        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs)), C.byref(self.handle)))
+        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n)),
+                             C.byref(self.handle)))
         info = _lib.Info()
         check(lib.okg_get_info(self.handle, C.byref(info)))
         self.info = info

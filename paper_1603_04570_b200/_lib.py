@@ -42,7 +42,7 @@ class Params(C.Structure):
         ("mg_cycles", C.c_int32), ("mg_pre", C.c_int32), ("mg_post", C.c_int32),
         ("mg_omega", C.c_double), ("min_coarse_size", C.c_int32),
         ("shat_perturb", C.c_double), ("max_dofs", C.c_int64),
-        ("device", C.c_int32), ("use_graphs", C.c_int32),
+        ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
     ]
 
 

@@ -78,6 +78,9 @@ static Op<DIM> dev_op(const HostOp& h) {
 struct Level {
   Grid g;
   HostOp shat;
+  bool tiled = false;
+  Tiling tl{};
+  unsigned tl_blocks = 0;
   double *b = nullptr, *x = nullptr, *ea = nullptr, *eb = nullptr, *res = nullptr;
 };
 
@@ -245,6 +248,60 @@ static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const
   note(c);
 }
 
+template <int DIM, int LOAD, int EPI>
+static void tiled(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
+  k_tiled<DIM, LOAD, EPI><<<L.tl_blocks, TileCfg<DIM>::NT, 0, c->stream>>>(L.g, dev_op<DIM>(op), L.tl, a);
+  note(c);
+}
+
+static TArgs targs(const double* x, const double* b, double* y, double* acc, double omega) {
+  TArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.x = x;
+  a.b = b;
+  a.y = y;
+  a.acc = acc;
+  a.omega = omega;
+  return a;
+}
+
+// core tiles + boundary list for one grid (okg_tiled.cuh)
+template <int DIM>
+static void make_tiling(okg_ctx* c, Level& L) {
+  const int n = L.g.n;
+  using TC = TileCfg<DIM>;
+  Tiling& t = L.tl;
+  t.ktiles = (n - 1 + TC::TK - 1) / TC::TK;
+  t.jtiles = DIM == 3 ? (n - 1 + TC::TJ - 1) / TC::TJ : 1;
+  const int base = t.ktiles * t.jtiles;
+  const int want = 148 * 8;
+  int nchunks = std::max(1, (want + base - 1) / base);
+  int ichunk = std::max(4, (n - 1 + nchunks - 1) / nchunks);
+  ichunk = std::min(ichunk, n - 1);
+  nchunks = (n - 1 + ichunk - 1) / ichunk;
+  t.ichunk = ichunk;
+  t.ncore = base * nchunks;
+  std::vector<uint32_t> bnd;
+  const int s = n + 1;
+  if (DIM == 3) {
+    for (int i = 0; i < s; ++i)
+      for (int j = 0; j < s; ++j)
+        for (int k = 0; k < s; ++k)
+          if (i == 0 || i == n || j == 0 || j == n || k == 0 || k == n)
+            bnd.push_back((uint32_t)((i * s + j) * s + k));
+  } else {
+    for (int i = 0; i < s; ++i)
+      for (int k = 0; k < s; ++k)
+        if (i == 0 || i == n || k == 0 || k == n) bnd.push_back((uint32_t)(i * s + k));
+  }
+  t.nbnd = (uint32_t)bnd.size();
+  double* d = dalloc(c, (bnd.size() + 1) / 2 + 1);
+  CK(cudaMemcpyAsync(d, bnd.data(), bnd.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+  t.bnd = reinterpret_cast<const uint32_t*>(d);
+  L.tl_blocks = (unsigned)t.ncore + (unsigned)((t.nbnd + TC::NT - 1) / TC::NT);
+  L.tiled = true;
+}
+
 static void axpy(okg_ctx* c, double a, const double* x, double* y, size_t n) {
   k_axpy<<<vblk(n), BS, 0, c->stream>>>(a, x, y, n);
   note(c);
@@ -282,38 +339,70 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   double* cur = L.ea;
   double* oth = L.eb;
   const int pre = c->p.mg_pre, post = c->p.mg_post;
+  // ---- pre-smoothing from zero (multigrid.hpp:102-104)
   if (pre == 0) {
     CK(cudaMemsetAsync(cur, 0, L.g.N * sizeof(double), c->stream));
   } else if (pre >= 2) {
-    k_pre2<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
-    note(c);
+    if (L.tiled) tiled<DIM, L_JAC0, T_JACOBI>(c, L, L.shat, targs(rhs, rhs, cur, nullptr, om));
+    else {
+      k_pre2<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
+      note(c);
+    }
     for (int s = 2; s < pre; ++s) {
-      op_apply<DIM>(c, L.g, L.shat, EPI_JACOBI, cur, rhs, oth, nullptr, om);
+      if (L.tiled) tiled<DIM, L_PLAIN, T_JACOBI>(c, L, L.shat, targs(cur, rhs, oth, nullptr, om));
+      else op_apply<DIM>(c, L.g, L.shat, EPI_JACOBI, cur, rhs, oth, nullptr, om);
       std::swap(cur, oth);
     }
   } else {
     k_jacobi0<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
     note(c);
   }
-  op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
+  // ---- residual, restriction, coarse correction (multigrid.hpp:106-110)
+  if (L.tiled) tiled<DIM, L_PLAIN, T_RESID>(c, L, L.shat, targs(cur, rhs, L.res, nullptr, 0.0));
+  else op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
   Level& C = c->lv[l + 1];
   k_restrict<DIM><<<nblk(C.g.N), BS, 0, c->stream>>>(L.g, C.g, L.res, C.b);
   note(c);
   mg_level<DIM>(c, l + 1, C.b, C.x, false);
-  k_prolong_add<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, C.g, C.x, cur);
-  note(c);
+  // ---- prolongation + post-smoothing (multigrid.hpp:111-115)
+  if (post == 0 || !L.tiled) {
+    k_prolong_add<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, C.g, C.x, cur);
+    note(c);
+  }
   for (int s = 0; s < post; ++s) {
-    if (s == post - 1) {
+    const bool lastsweep = (s == post - 1);
+    if (L.tiled) {
+      TArgs a = targs(cur, rhs, lastsweep ? nullptr : oth, lastsweep ? out : nullptr, om);
+      if (s == 0) {  // stage e + P e_c: the correction is fused into this sweep
+        a.x2 = C.x;
+        a.gc = C.g;
+        if (!lastsweep) tiled<DIM, L_PROLONG, T_JACOBI>(c, L, L.shat, a);
+        else if (acc) tiled<DIM, L_PROLONG, T_JACOBI_ACC>(c, L, L.shat, a);
+        else tiled<DIM, L_PROLONG, T_JACOBI_SET>(c, L, L.shat, a);
+      } else {
+        if (!lastsweep) tiled<DIM, L_PLAIN, T_JACOBI>(c, L, L.shat, a);
+        else if (acc) tiled<DIM, L_PLAIN, T_JACOBI_ACC>(c, L, L.shat, a);
+        else tiled<DIM, L_PLAIN, T_JACOBI_SET>(c, L, L.shat, a);
+      }
+    } else if (lastsweep) {
       op_apply<DIM>(c, L.g, L.shat, acc ? EPI_JACOBI_ACC : EPI_JACOBI_SET, cur, rhs, nullptr, out, om);
     } else {
       op_apply<DIM>(c, L.g, L.shat, EPI_JACOBI, cur, rhs, oth, nullptr, om);
-      std::swap(cur, oth);
     }
+    if (!lastsweep) std::swap(cur, oth);
   }
   if (post == 0) {
     if (acc) axpy(c, 1.0, cur, out, L.g.N);
     else copy(c, cur, out, L.g.N);
   }
+}
+
+// plain apply y = A x on level l (tiled when the level is)
+template <int DIM>
+static void apply_level(okg_ctx* c, int l, const HostOp& op, const double* x, double* y) {
+  const Level& L = c->lv[l];
+  if (L.tiled) tiled<DIM, L_PLAIN, T_APPLY>(c, L, op, targs(x, nullptr, y, nullptr, 0.0));
+  else op_apply<DIM>(c, L.g, op, EPI_APPLY, x, nullptr, y, nullptr);
 }
 
 // apply_shat_inv (multigrid.hpp:133-149): `cycles` V-cycles composed by Richardson
@@ -323,7 +412,8 @@ static void shat_inv(okg_ctx* c, const double* b, double* x, int cycles) {
     const double* rhs = cyc == 0 ? b : c->shr;
     mg_level<DIM>(c, 0, rhs, x, cyc > 0);
     if (cyc + 1 == cycles) break;
-    op_apply<DIM>(c, c->lv[0].g, c->lv[0].shat, EPI_RESID, x, b, c->shr, nullptr);
+    if (c->lv[0].tiled) tiled<DIM, L_PLAIN, T_RESID>(c, c->lv[0], c->lv[0].shat, targs(x, b, c->shr, nullptr, 0.0));
+    else op_apply<DIM>(c, c->lv[0].g, c->lv[0].shat, EPI_RESID, x, b, c->shr, nullptr);
   }
 }
 
@@ -343,9 +433,19 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
   }
   for (int j = 0; j + 1 < k; ++j) {
     const int last = (j == k - 2);
-    k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
-                                                      c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last);
-    note(c);
+    if (c->lv[0].tiled) {
+      TArgs a = targs(dcur, j == 0 ? b : c->cr, c->cr, x, 0.0);
+      a.x2 = j == 0 ? dcur : x;
+      a.y2 = dnxt;
+      a.c1 = c->cheb_c1[j];
+      a.c2 = c->cheb_c2[j];
+      a.last = last;
+      tiled<DIM, L_PLAIN, T_CHEB>(c, c->lv[0], A, a);
+    } else {
+      k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
+                                                        c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last);
+      note(c);
+    }
     std::swap(dcur, dnxt);
   }
 }
@@ -373,14 +473,14 @@ static void capply(okg_ctx* c, const double* x, const double* v, const double* b
 template <int DIM>
 static void schur_tilde_inv(okg_ctx* c, const double* b, double* x) {
   shat_inv<DIM>(c, b, c->sy, c->p.mg_cycles);
-  op_apply<DIM>(c, c->fine, c->M, EPI_APPLY, c->sy, nullptr, c->st, nullptr);
+  apply_level<DIM>(c, 0, c->M, c->sy, c->st);
   shat_inv<DIM>(c, c->st, x, c->p.mg_cycles);
 }
 
 // apply_schur (precond.hpp:210-222); resid: y = b - S v
 template <int DIM>
 static void apply_schur(okg_ctx* c, const double* v, const double* b, double* y) {
-  op_apply<DIM>(c, c->fine, c->K, EPI_APPLY, v, nullptr, c->kv, nullptr);
+  apply_level<DIM>(c, 0, c->K, v, c->kv);
   cheb<DIM>(c, c->M, c->kv, c->zz);
   if (b) capply<DIM, CM_SCHUR_RES>(c, c->zz, v, b, y, c->c);
   else capply<DIM, CM_SCHUR>(c, c->zz, v, nullptr, y, c->c);
@@ -818,6 +918,11 @@ static void build(okg_ctx* c) {
       L.eb = dalloc(c, nl);
       L.res = dalloc(c, nl);
     }
+    // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
+    const int tmin = p.tiled_min_n == 0 ? (DIM == 3 ? 32 : 128) : p.tiled_min_n;
+    if (tmin > 0)
+      for (Level& L : c->lv)
+        if (L.g.n >= std::max(tmin, 2)) make_tiling<DIM>(c, L);
     // coarsest: dense SPD inverse (replaces CholeskyFactor, multigrid.hpp:82-83)
     Level& Lc = c->lv.back();
     const int nc = (int)Lc.g.N;
@@ -985,12 +1090,12 @@ template <int DIM>
 static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double* y) {
   const int nlev = static_cast<int>(c->lv.size());
   switch (kind) {
-    case OKG_OP_M: op_apply<DIM>(c, c->fine, c->M, EPI_APPLY, x, nullptr, y, nullptr); break;
-    case OKG_OP_K: op_apply<DIM>(c, c->fine, c->K, EPI_APPLY, x, nullptr, y, nullptr); break;
-    case OKG_OP_A: op_apply<DIM>(c, c->fine, c->A, EPI_APPLY, x, nullptr, y, nullptr); break;
+    case OKG_OP_M: apply_level<DIM>(c, 0, c->M, x, y); break;
+    case OKG_OP_K: apply_level<DIM>(c, 0, c->K, x, y); break;
+    case OKG_OP_A: apply_level<DIM>(c, 0, c->A, x, y); break;
     case OKG_OP_SHAT:
       if (level < 0 || level >= nlev) THROW(OKG_EINVAL, "level out of range");
-      op_apply<DIM>(c, c->lv[level].g, c->lv[level].shat, EPI_APPLY, x, nullptr, y, nullptr);
+      apply_level<DIM>(c, level, c->lv[level].shat, x, y);
       break;
     case OKG_OP_PROLONG:
       if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
@@ -1357,18 +1462,40 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
   // operands: reuse workspace vectors (contents are finite)
   double *x = c->cd0, *b = c->cd1, *y = c->cr, *z = c->kv;
   auto launch = [&]() {
+    const bool T = L0.tiled;
     switch (which) {
-      case OKG_KT_SMOOTH: op_apply<DIM>(c, g, L0.shat, EPI_JACOBI, x, b, y, nullptr, om); break;
-      case OKG_KT_RESID: op_apply<DIM>(c, g, L0.shat, EPI_RESID, x, b, y, nullptr); break;
-      case OKG_KT_PRE2:
-        k_pre2<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(L0.shat), b, y, om);
-        note(c);
+      case OKG_KT_SMOOTH:
+        if (T) tiled<DIM, L_PLAIN, T_JACOBI>(c, L0, L0.shat, targs(x, b, y, nullptr, om));
+        else op_apply<DIM>(c, g, L0.shat, EPI_JACOBI, x, b, y, nullptr, om);
         break;
-      case OKG_KT_POST_ACC: op_apply<DIM>(c, g, L0.shat, EPI_JACOBI_ACC, x, b, nullptr, z, om); break;
+      case OKG_KT_RESID:
+        if (T) tiled<DIM, L_PLAIN, T_RESID>(c, L0, L0.shat, targs(x, b, y, nullptr, 0.0));
+        else op_apply<DIM>(c, g, L0.shat, EPI_RESID, x, b, y, nullptr);
+        break;
+      case OKG_KT_PRE2:
+        if (T) tiled<DIM, L_JAC0, T_JACOBI>(c, L0, L0.shat, targs(b, b, y, nullptr, om));
+        else {
+          k_pre2<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(L0.shat), b, y, om);
+          note(c);
+        }
+        break;
+      case OKG_KT_POST_ACC:
+        if (T) tiled<DIM, L_PLAIN, T_JACOBI_ACC>(c, L0, L0.shat, targs(x, b, nullptr, z, om));
+        else op_apply<DIM>(c, g, L0.shat, EPI_JACOBI_ACC, x, b, nullptr, z, om);
+        break;
       case OKG_KT_CHEB:
-        k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(c->A), x, b, y, z, c->zz, c->rr,
-                                                          c->cheb_c1[0], c->cheb_c2[0], 0);
-        note(c);
+        if (T) {
+          TArgs a = targs(x, b, y, z, 0.0);
+          a.x2 = c->zz;
+          a.y2 = c->rr;
+          a.c1 = c->cheb_c1[0];
+          a.c2 = c->cheb_c2[0];
+          tiled<DIM, L_PLAIN, T_CHEB>(c, L0, c->A, a);
+        } else {
+          k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(c->A), x, b, y, c->zz, c->rr, z,
+                                                            c->cheb_c1[0], c->cheb_c2[0], 0);
+          note(c);
+        }
         break;
       case OKG_KT_JACOBIAN: jacobian<DIM>(c, c->pz, c->pw); break;
       case OKG_KT_RESTRICT:
@@ -1376,8 +1503,15 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
         note(c);
         break;
       case OKG_KT_PROLONG:
-        k_prolong_add<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, c->lv[1].g, c->lv[1].x, y);
-        note(c);
+        if (T) {
+          TArgs a = targs(x, b, y, nullptr, om);
+          a.x2 = c->lv[1].x;
+          a.gc = c->lv[1].g;
+          tiled<DIM, L_PROLONG, T_JACOBI>(c, L0, L0.shat, a);
+        } else {
+          k_prolong_add<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, c->lv[1].g, c->lv[1].x, y);
+          note(c);
+        }
         break;
       default: THROW(OKG_EINVAL, "okg_kernel_timing: unknown kernel %d", which);
     }
@@ -1393,7 +1527,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
     case OKG_KT_CHEB: *bytes = 6 * N * B; break;
     case OKG_KT_JACOBIAN: *bytes = (4 + npos) * N * B; break;
     case OKG_KT_RESTRICT: *bytes = (N + Nc) * B; break;
-    case OKG_KT_PROLONG: *bytes = (2 * N + Nc) * B; break;
+    case OKG_KT_PROLONG: *bytes = (L0.tiled ? 3 * N + Nc : 2 * N + Nc) * B; break;
   }
   bool had_lin = c->have_lin;
   for (int i = 0; i < 3; ++i) launch();

@@ -22,6 +22,7 @@
 #include <utility>
 
 #include "okg_common.cuh"
+#include "okg_tiled.cuh"
 
 namespace okg {
 

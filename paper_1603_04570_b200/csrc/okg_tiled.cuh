@@ -1,0 +1,211 @@
+// okg_tiled.cuh -- 2.5D shared-memory tiled stencil kernels for the large
+// multigrid levels (the V-cycle is ~80% of a Newton step).
+//
+// Why: the naive one-thread-per-vertex gather issues 15 (3D) global loads per
+// vertex; the L1/L2 traffic is ~7x the DRAM traffic and boundary vertices
+// make whole warps diverge.  Here a CTA owns a (TJ x TK) tile of the (y,z)
+// plane of *interior* vertices and marches along x (the slowest index),
+// staging the tile + 1-vertex halo of plane x+1 in a 4-slot shared-memory
+// ring, so every operand value is read from L2 about once.  Boundary vertices
+// (any coordinate 0 or n, ~6/n of the grid) are handled by extra CTAs from a
+// precomputed index list with the per-class weight table.
+//
+// The staging ("loader") step can transform the operand on its way into
+// shared memory, which is how two passes are fused away:
+//   L_JAC0   stages e1 = w D^-1 r   -> first two damped-Jacobi sweeps in one
+//                                      pass (multigrid.hpp:103-104)
+//   L_PROLONG stages e + P e_c      -> coarse-grid correction fused into the
+//                                      first post-smoothing sweep
+//                                      (multigrid.hpp:111-115)
+// In 2D the "plane" is a row segment of TK vertices marching along x.
+#pragma once
+#include "okg_common.cuh"
+
+namespace okg {
+
+template <int DIM>
+struct TileCfg;
+template <>
+struct TileCfg<3> {
+  static constexpr int TK = 32, TJ = 8, NT = TK * TJ;
+  static constexpr int PW = TK + 2, PH = TJ + 2, PSZ = PW * PH;
+};
+template <>
+struct TileCfg<2> {
+  static constexpr int TK = 256, TJ = 1, NT = TK * TJ;
+  static constexpr int PW = TK + 2, PH = 1, PSZ = PW;
+};
+
+struct Tiling {
+  int32_t ncore;    // core CTAs
+  int32_t ktiles, jtiles, ichunk;  // tiles along z, y; planes per CTA along x
+  uint32_t nbnd;    // boundary vertices
+  const uint32_t* __restrict__ bnd;  // boundary vertex indices
+};
+
+enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2 };
+enum TEpi {
+  T_APPLY = 0,       // y = A s
+  T_RESID = 1,       // y = b - A s
+  T_JACOBI = 2,      // y = s + w D^-1 (b - A s)
+  T_JACOBI_SET = 3,  // acc = s + w D^-1 (b - A s)
+  T_JACOBI_ACC = 4,  // acc += s + w D^-1 (b - A s)
+  T_CHEB = 5         // Chebyshev step (see k_cheb_step)
+};
+
+struct TArgs {
+  const double* x;   // staged operand (x, r, d or e)
+  const double* b;   // rhs / r_in
+  double* y;         // output / r_out
+  double* acc;       // accumulation target / x_out
+  const double* x2;  // x_in (cheb) / e_c (prolong)
+  double* y2;        // d_out (cheb)
+  double omega, c1, c2;
+  int32_t last;
+  Grid gc;           // coarse grid (L_PROLONG)
+};
+
+// class digit of a coordinate
+__device__ __forceinline__ int cdig(int v, int n) { return v == 0 ? 0 : (v == n ? 2 : 1); }
+
+template <int DIM>
+__device__ __forceinline__ int class_of(const Grid& g, int i, int j, int k) {
+  return DIM == 3 ? cdig(i, g.n) * 9 + cdig(j, g.n) * 3 + cdig(k, g.n) : cdig(i, g.n) * 3 + cdig(k, g.n);
+}
+
+// prolongation value (P e_c) at fine vertex (i, j, k) (mesh.hpp:169-194)
+template <int DIM>
+__device__ __forceinline__ double prolong_at(const Grid& gc, const double* __restrict__ ec, int i, int j, int k) {
+  const int li = i >> 1, lj = j >> 1, lk = k >> 1;
+  const int hi = (i + 1) >> 1, hj = (j + 1) >> 1, hk = (k + 1) >> 1;
+  const uint32_t lo = DIM == 3 ? (uint32_t)li * gc.ps + (uint32_t)lj * gc.s + lk : (uint32_t)li * gc.s + lk;
+  const uint32_t up = DIM == 3 ? (uint32_t)hi * gc.ps + (uint32_t)hj * gc.s + hk : (uint32_t)hi * gc.s + hk;
+  if (lo == up) return __ldg(ec + lo);
+  return fma(0.5, __ldg(ec + up), 0.5 * __ldg(ec + lo));
+}
+
+// staged value of vertex (i,j,k) (linear index v)
+template <int DIM, int LOAD>
+__device__ __forceinline__ double stage_val(const Grid& g, const Op<DIM>& op, const TArgs& a, uint32_t v, int i,
+                                            int j, int k) {
+  if (LOAD == L_PLAIN) return __ldg(a.x + v);
+  if (LOAD == L_JAC0) {
+    const int cls = class_of<DIM>(g, i, j, k);
+    const double invd =
+        cls == Traits<DIM>::INTERIOR ? op.invd : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+    return a.omega * invd * __ldg(a.x + v);
+  }
+  // L_PROLONG: e + P e_c  (x + t, t rounded first: multigrid.hpp:111-112)
+  const double t = prolong_at<DIM>(a.gc, a.x2, i, j, k);
+  return __ldg(a.x + v) + t;
+}
+
+template <int DIM, int EPI>
+__device__ __forceinline__ void epilogue(const TArgs& a, uint32_t idx, double s_own, double As, double invd) {
+  if (EPI == T_APPLY) {
+    a.y[idx] = As;
+  } else if (EPI == T_RESID) {
+    a.y[idx] = a.b[idx] - As;
+  } else if (EPI == T_CHEB) {
+    // r = r_in - A d ; z = r D^-1 ; d' = c1 d + c2 z ; x_out = x_in + d'
+    const double r = a.b[idx] - As;
+    const double z = r * invd;
+    const double dn = a.c1 * s_own + a.c2 * z;
+    a.acc[idx] = a.x2[idx] + dn;
+    if (!a.last) {
+      a.y2[idx] = dn;
+      a.y[idx] = r;
+    }
+  } else {
+    const double e = s_own + a.omega * invd * (a.b[idx] - As);
+    if (EPI == T_JACOBI) a.y[idx] = e;
+    else if (EPI == T_JACOBI_SET) a.acc[idx] = e;
+    else a.acc[idx] = a.acc[idx] + e;
+  }
+}
+
+template <int DIM, int LOAD, int EPI>
+__global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
+  using TC = TileCfg<DIM>;
+  constexpr int NO = Traits<DIM>::NOFF;
+  const int tid = threadIdx.x;
+  if ((int)blockIdx.x >= tl.ncore) {
+    // ---- boundary vertices: class-table path ----
+    const uint32_t t = (blockIdx.x - tl.ncore) * TC::NT + tid;
+    if (t >= tl.nbnd) return;
+    const uint32_t idx = __ldg(tl.bnd + t);
+    const Node<DIM> nd = locate<DIM>(g, idx);
+    const double* w = op.tab + nd.cls * (NO + 1);
+    double As = 0.0, s_own = 0.0;
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      const int di = off_comp(DIM, o, 0);
+      const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
+      const int dk = off_comp(DIM, o, DIM - 1);
+      const int ni = nd.i + di;
+      const int nj = DIM == 3 ? nd.j + dj : 0;
+      const int nk = (DIM == 3 ? nd.k : nd.j) + dk;  // fastest coordinate
+      if (ni < 0 || ni > g.n || nk < 0 || nk > g.n || (DIM == 3 && (nj < 0 || nj > g.n))) continue;
+      const uint32_t v = (uint32_t)((int)idx + g.off[o]);
+      const double sv = stage_val<DIM, LOAD>(g, op, a, v, ni, nj, nk);
+      if (o == Traits<DIM>::CENTER) s_own = sv;
+      const double wo = __ldg(w + o);
+      if (wo != 0.0) As = fma(wo, sv, As);
+    }
+    epilogue<DIM, EPI>(a, idx, s_own, As, __ldg(w + NO));
+    return;
+  }
+  // ---- core tile marching along x ----
+  __shared__ double ring[4][TC::PSZ];
+  int b = blockIdx.x;
+  const int kt = b % tl.ktiles;
+  b /= tl.ktiles;
+  const int jt = DIM == 3 ? b % tl.jtiles : 0;
+  const int ic = DIM == 3 ? b / tl.jtiles : b;
+  const int k0 = 1 + kt * TC::TK;
+  const int j0 = DIM == 3 ? 1 + jt * TC::TJ : 0;
+  const int i0 = 1 + ic * tl.ichunk;
+  const int i1 = min(i0 + tl.ichunk, g.n);
+  const int tk = tid % TC::TK, tj = tid / TC::TK;
+  const int k = k0 + tk, j = j0 + tj;
+  const bool active = k <= g.n - 1 && (DIM == 2 || j <= g.n - 1);
+
+  auto load_plane = [&](int ip) {
+    double* dst = ring[ip & 3];
+    for (int e = tid; e < TC::PSZ; e += TC::NT) {
+      const int hj = DIM == 3 ? e / TC::PW : 0;
+      const int hk = DIM == 3 ? e - hj * TC::PW : e;
+      const int gj = DIM == 3 ? j0 - 1 + hj : 0;
+      const int gk = k0 - 1 + hk;
+      double v = 0.0;
+      if (gk <= g.n && gj <= g.n) {
+        const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
+        v = stage_val<DIM, LOAD>(g, op, a, lin, ip, gj, gk);
+      }
+      dst[e] = v;
+    }
+  };
+  load_plane(i0 - 1);
+  load_plane(i0);
+  for (int i = i0; i < i1; ++i) {
+    load_plane(i + 1);
+    __syncthreads();
+    if (active) {
+      double As = 0.0;
+      double s_own = 0.0;
+#pragma unroll
+      for (int o = 0; o < NO; ++o) {
+        const int di = off_comp(DIM, o, 0);
+        const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
+        const int dk = off_comp(DIM, o, DIM - 1);
+        const double sv = ring[(i + di) & 3][DIM == 3 ? (tj + 1 + dj) * TC::PW + (tk + 1 + dk) : tk + 1 + dk];
+        if (o == Traits<DIM>::CENTER) s_own = sv;
+        As = fma(op.w[o], sv, As);
+      }
+      const uint32_t idx = DIM == 3 ? (uint32_t)i * g.ps + (uint32_t)j * g.s + k : (uint32_t)i * g.s + k;
+      epilogue<DIM, EPI>(a, idx, s_own, As, op.invd);
+    }
+  }
+}
+
+}  // namespace okg
