@@ -16,3 +16,4 @@ if [ "${NCU:-1}" = "1" ]; then
     echo "ncu rc=$?"; tail -2 gpurun_out/ncu.log
   fi
 fi
+if [ "${PROBE:-0}" = "1" ]; then timeout 600 python tools/gpu_probe.py --big ${BIG:-3:64,2:512,3:128,2:2048} > gpurun_out/probe.log 2>&1; echo "probe rc=$?"; grep -E "timing|step" gpurun_out/probe.log | tail -20; fi
