@@ -61,6 +61,9 @@ typedef struct okg_params {
   int32_t use_graphs;       /* capture the Arnoldi operator in a CUDA graph (default 1) */
   int32_t tiled_min_n;      /* levels with n >= this use the shared-memory tiled stencil
                                kernels; 0 = default (3D: 32, 2D: 128), < 0 = never */
+  int32_t tail_max_vertices;/* multigrid levels (below the finest) with at most this many
+                               vertices run as ONE single-CTA V-cycle kernel;
+                               0 = default (6000), < 0 = never */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -96,6 +99,8 @@ typedef struct okg_info {
   double c, sqrt_c, a_coeff, dt_theta, lambda_lo, lambda_hi, eps_sqrt_c;
   int64_t device_bytes;       /* device memory held by the context        */
   int32_t graph_nodes;        /* kernels in the captured Arnoldi graph    */
+  int32_t tail_start;         /* first level of the single-CTA tail (-1: none) */
+  int32_t tiled_mask;         /* bit l set: level l uses the tiled kernels */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */

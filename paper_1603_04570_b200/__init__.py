@@ -70,7 +70,7 @@ class SolverConfig:
         return s ** self.dim
 
     def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
-                  tiled_min_n: int = 0) -> _lib.Params:
+                  tiled_min_n: int = 0, tail_max_vertices: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -81,6 +81,7 @@ class SolverConfig:
         p.device = device
         p.use_graphs = 1 if use_graphs else 0
         p.tiled_min_n = tiled_min_n
+        p.tail_max_vertices = tail_max_vertices
         return p
 
     def validate(self) -> None:
@@ -228,13 +229,13 @@ class DeviceArray:
 # --------------------------------------------------------------------------------------
 class SchurContext:
     def __init__(self, cfg: SolverConfig, device: int = 0, shat_perturb: float = 0.0,
-                 use_graphs: bool = True, tiled_min_n: int = 0):
+                 use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0):
         if cfg.cheby_precond != "jacobi":
             raise ConfigError("schur context: only cheby_precond = 'jacobi' is implemented on the GPU path")
         self.cfg = cfg
         self.device = device
         self.handle = C.c_void_p()
-        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n)),
+        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices)),
                              C.byref(self.handle)))
         info = _lib.Info()
         check(lib.okg_get_info(self.handle, C.byref(info)))
@@ -253,6 +254,8 @@ class SchurContext:
         self.level_n = [int(info.level_n[i]) for i in range(self.levels)]
         self.device_bytes = int(info.device_bytes)
         self.graph_nodes = int(info.graph_nodes)
+        self.tail_start = int(info.tail_start)
+        self.tiled_levels = [l for l in range(self.levels) if (info.tiled_mask >> l) & 1]
         self.Me_set = False
 
     def rows(self) -> int:

@@ -43,6 +43,7 @@ class Params(C.Structure):
         ("mg_omega", C.c_double), ("min_coarse_size", C.c_int32),
         ("shat_perturb", C.c_double), ("max_dofs", C.c_int64),
         ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
+        ("tail_max_vertices", C.c_int32),
     ]
 
 
@@ -69,6 +70,7 @@ class Info(C.Structure):
         ("c", C.c_double), ("sqrt_c", C.c_double), ("a_coeff", C.c_double),
         ("dt_theta", C.c_double), ("lambda_lo", C.c_double), ("lambda_hi", C.c_double),
         ("eps_sqrt_c", C.c_double), ("device_bytes", C.c_int64), ("graph_nodes", C.c_int32),
+        ("tail_start", C.c_int32), ("tiled_mask", C.c_int32),
     ]
 
 

@@ -102,6 +102,7 @@ struct okg_ctx {
   std::vector<Level> lv;
   int nc = 0;
   double* Ainv = nullptr;
+  int tail_start = -1;  // first level run by the single-CTA tail kernel (-1: none)
   double b_int = 0;
   double* b_tab = nullptr;
   Nonlin nl;
@@ -248,10 +249,23 @@ static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const
   note(c);
 }
 
+template <int DIM, int LOAD, int EPI, int TI>
+static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
+  static bool attr = false;  // dynamic smem above 48 KB needs an opt-in (per kernel instance)
+  const size_t smem = (size_t)(TI + 2) * TileCfg<DIM>::PSZ * sizeof(double);
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_tiled<DIM, LOAD, EPI, TI><<<L.tl_blocks, TileCfg<DIM>::NT, smem, c->stream>>>(L.g, dev_op<DIM>(op), L.tl, a);
+  note(c);
+}
+
 template <int DIM, int LOAD, int EPI>
 static void tiled(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
-  k_tiled<DIM, LOAD, EPI><<<L.tl_blocks, TileCfg<DIM>::NT, 0, c->stream>>>(L.g, dev_op<DIM>(op), L.tl, a);
-  note(c);
+  if (L.tl.ichunk == 8) tiled_ti<DIM, LOAD, EPI, 8>(c, L, op, a);
+  else if (L.tl.ichunk == 4) tiled_ti<DIM, LOAD, EPI, 4>(c, L, op, a);
+  else tiled_ti<DIM, LOAD, EPI, 2>(c, L, op, a);
 }
 
 static TArgs targs(const double* x, const double* b, double* y, double* acc, double omega) {
@@ -274,11 +288,10 @@ static void make_tiling(okg_ctx* c, Level& L) {
   t.ktiles = (n - 1 + TC::TK - 1) / TC::TK;
   t.jtiles = DIM == 3 ? (n - 1 + TC::TJ - 1) / TC::TJ : 1;
   const int base = t.ktiles * t.jtiles;
-  const int want = 148 * 8;
-  int nchunks = std::max(1, (want + base - 1) / base);
-  int ichunk = std::max(4, (n - 1 + nchunks - 1) / nchunks);
-  ichunk = std::min(ichunk, n - 1);
-  nchunks = (n - 1 + ichunk - 1) / ichunk;
+  // vertices per thread along x (TI): as deep as possible while keeping >= ~4 CTAs per SM
+  int ichunk = 8;
+  while (ichunk > 2 && base * ((n - 1 + ichunk - 1) / ichunk) < 148 * 4) ichunk /= 2;
+  const int nchunks = (n - 1 + ichunk - 1) / ichunk;
   t.ichunk = ichunk;
   t.ncore = base * nchunks;
   std::vector<uint32_t> bnd;
@@ -321,10 +334,41 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
   note(c);
 }
 
+// levels tail_start..coarsest in one single-CTA launch (okg_tail.cuh)
+template <int DIM>
+static void run_tail(okg_ctx* c, int l0, const double* rhs, double* out) {
+  TailArgs<DIM> A;
+  std::memset(&A, 0, sizeof A);
+  A.nl = static_cast<int>(c->lv.size()) - l0;
+  for (int q = 0; q < A.nl; ++q) {
+    Level& L = c->lv[l0 + q];
+    A.L[q].g = L.g;
+    A.L[q].op = dev_op<DIM>(L.shat);
+    A.L[q].b = L.b;
+    A.L[q].x = L.x;
+    A.L[q].ea = L.ea;
+    A.L[q].eb = L.eb;
+    A.L[q].res = L.res;
+  }
+  A.pre = c->p.mg_pre;
+  A.post = c->p.mg_post;
+  A.omega = c->p.mg_omega;
+  A.rhs = rhs;
+  A.out = out;
+  A.Ainv = c->Ainv;
+  A.nc = c->nc;
+  k_vcycle_tail<DIM><<<1, TAIL_NT, 0, c->stream>>>(A);
+  note(c);
+}
+
 template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
   Level& L = c->lv[l];
   const int last = static_cast<int>(c->lv.size()) - 1;
+  if (l == c->tail_start && !acc && l > 0) {
+    run_tail<DIM>(c, l, rhs, out);
+    return;
+  }
   if (l == last) {
     if (!acc) {
       coarse_solve<DIM>(c, rhs, out);
@@ -918,6 +962,15 @@ static void build(okg_ctx* c) {
       L.eb = dalloc(c, nl);
       L.res = dalloc(c, nl);
     }
+    // single-CTA tail for the small levels (okg_tail.cuh)
+    const int64_t tmax = p.tail_max_vertices == 0 ? 6000 : p.tail_max_vertices;
+    if (tmax > 0) {
+      for (size_t l = 1; l < c->lv.size(); ++l)
+        if ((int64_t)c->lv[l].g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL) {
+          c->tail_start = (int)l;
+          break;
+        }
+    }
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
     const int tmin = p.tiled_min_n == 0 ? (DIM == 3 ? 32 : 128) : p.tiled_min_n;
     if (tmin > 0)
@@ -1295,6 +1348,9 @@ int okg_get_info(okg_ctx* c, okg_info* info) {
   info->eps_sqrt_c = c->eps_sqrt_c;
   info->device_bytes = static_cast<int64_t>(c->bytes);
   info->graph_nodes = c->arn_nodes;
+  info->tail_start = c->tail_start;
+  for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
+    if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
   return OKG_OK;
 }
 

@@ -23,6 +23,7 @@
 
 #include "okg_common.cuh"
 #include "okg_tiled.cuh"
+#include "okg_tail.cuh"
 
 namespace okg {
 

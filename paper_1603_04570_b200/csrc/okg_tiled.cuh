@@ -17,7 +17,7 @@
 //   L_PROLONG stages e + P e_c      -> coarse-grid correction fused into the
 //                                      first post-smoothing sweep
 //                                      (multigrid.hpp:111-115)
-// In 2D the "plane" is a row segment of TK vertices marching along x.
+// In 2D the "plane" is a row segment of TK vertices.
 #pragma once
 #include "okg_common.cuh"
 
@@ -38,7 +38,7 @@ struct TileCfg<2> {
 
 struct Tiling {
   int32_t ncore;    // core CTAs
-  int32_t ktiles, jtiles, ichunk;  // tiles along z, y; planes per CTA along x
+  int32_t ktiles, jtiles, ichunk;  // tiles along z, y; planes per CTA along x (= TI)
   uint32_t nbnd;    // boundary vertices
   const uint32_t* __restrict__ bnd;  // boundary vertex indices
 };
@@ -100,31 +100,41 @@ __device__ __forceinline__ double stage_val(const Grid& g, const Op<DIM>& op, co
   return __ldg(a.x + v) + t;
 }
 
+// pointwise operands each epilogue needs (prefetched before the barrier)
+template <int EPI>
+struct EpiNeeds {
+  static constexpr bool B = EPI != T_APPLY;
+  static constexpr bool P2 = EPI == T_JACOBI_ACC || EPI == T_CHEB;  // acc / x_in
+};
+
 template <int DIM, int EPI>
-__device__ __forceinline__ void epilogue(const TArgs& a, uint32_t idx, double s_own, double As, double invd) {
+__device__ __forceinline__ void epilogue_pre(const TArgs& a, uint32_t idx, double s_own, double As, double invd,
+                                             double bv, double pv) {
   if (EPI == T_APPLY) {
     a.y[idx] = As;
   } else if (EPI == T_RESID) {
-    a.y[idx] = a.b[idx] - As;
+    a.y[idx] = bv - As;
   } else if (EPI == T_CHEB) {
-    // r = r_in - A d ; z = r D^-1 ; d' = c1 d + c2 z ; x_out = x_in + d'
-    const double r = a.b[idx] - As;
+    const double r = bv - As;
     const double z = r * invd;
     const double dn = a.c1 * s_own + a.c2 * z;
-    a.acc[idx] = a.x2[idx] + dn;
+    a.acc[idx] = pv + dn;
     if (!a.last) {
       a.y2[idx] = dn;
       a.y[idx] = r;
     }
   } else {
-    const double e = s_own + a.omega * invd * (a.b[idx] - As);
+    const double e = s_own + a.omega * invd * (bv - As);
     if (EPI == T_JACOBI) a.y[idx] = e;
     else if (EPI == T_JACOBI_SET) a.acc[idx] = e;
-    else a.acc[idx] = a.acc[idx] + e;
+    else a.acc[idx] = pv + e;
   }
 }
 
-template <int DIM, int LOAD, int EPI>
+// Core CTAs: a (TI+2) x (TJ+2) x (TK+2) tile (3D) or (TI+2) x (TK+2) (2D) of
+// staged values is loaded with all global loads in flight at once, then each
+// thread computes TI vertices along x.  Extra CTAs take the boundary list.
+template <int DIM, int LOAD, int EPI, int TI>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
   using TC = TileCfg<DIM>;
   constexpr int NO = Traits<DIM>::NOFF;
@@ -152,11 +162,13 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
       const double wo = __ldg(w + o);
       if (wo != 0.0) As = fma(wo, sv, As);
     }
-    epilogue<DIM, EPI>(a, idx, s_own, As, __ldg(w + NO));
+    const double bv = EpiNeeds<EPI>::B ? a.b[idx] : 0.0;
+    const double pv = EPI == T_CHEB ? a.x2[idx] : (EPI == T_JACOBI_ACC ? a.acc[idx] : 0.0);
+    epilogue_pre<DIM, EPI>(a, idx, s_own, As, __ldg(w + NO), bv, pv);
     return;
   }
-  // ---- core tile marching along x ----
-  __shared__ double ring[4][TC::PSZ];
+  // ---- core tile ----
+  extern __shared__ double tile[];
   int b = blockIdx.x;
   const int kt = b % tl.ktiles;
   b /= tl.ktiles;
@@ -164,47 +176,67 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
   const int ic = DIM == 3 ? b / tl.jtiles : b;
   const int k0 = 1 + kt * TC::TK;
   const int j0 = DIM == 3 ? 1 + jt * TC::TJ : 0;
-  const int i0 = 1 + ic * tl.ichunk;
-  const int i1 = min(i0 + tl.ichunk, g.n);
+  const int i0 = 1 + ic * TI;
+  const int ni = min(TI, g.n - i0);  // planes computed by this CTA
   const int tk = tid % TC::TK, tj = tid / TC::TK;
   const int k = k0 + tk, j = j0 + tj;
   const bool active = k <= g.n - 1 && (DIM == 2 || j <= g.n - 1);
-
-  auto load_plane = [&](int ip) {
-    double* dst = ring[ip & 3];
-    for (int e = tid; e < TC::PSZ; e += TC::NT) {
-      const int hj = DIM == 3 ? e / TC::PW : 0;
-      const int hk = DIM == 3 ? e - hj * TC::PW : e;
-      const int gj = DIM == 3 ? j0 - 1 + hj : 0;
-      const int gk = k0 - 1 + hk;
-      double v = 0.0;
-      if (gk <= g.n && gj <= g.n) {
-        const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
-        v = stage_val<DIM, LOAD>(g, op, a, lin, ip, gj, gk);
-      }
-      dst[e] = v;
-    }
-  };
-  load_plane(i0 - 1);
-  load_plane(i0);
-  for (int i = i0; i < i1; ++i) {
-    load_plane(i + 1);
-    __syncthreads();
-    if (active) {
-      double As = 0.0;
-      double s_own = 0.0;
+  const uint32_t idx0 = DIM == 3 ? (uint32_t)i0 * g.ps + (uint32_t)j * g.s + k : (uint32_t)i0 * g.s + k;
+  const uint32_t pstride = DIM == 3 ? g.ps : (uint32_t)g.s;
+  // prefetch the pointwise operands of this thread's TI vertices
+  double pb[TI], pp[TI];
 #pragma unroll
-      for (int o = 0; o < NO; ++o) {
-        const int di = off_comp(DIM, o, 0);
-        const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
-        const int dk = off_comp(DIM, o, DIM - 1);
-        const double sv = ring[(i + di) & 3][DIM == 3 ? (tj + 1 + dj) * TC::PW + (tk + 1 + dk) : tk + 1 + dk];
-        if (o == Traits<DIM>::CENTER) s_own = sv;
-        As = fma(op.w[o], sv, As);
+  for (int t = 0; t < TI; ++t) {
+    const bool ok = active && t < ni;
+    const uint32_t idx = idx0 + (uint32_t)t * pstride;
+    pb[t] = (EpiNeeds<EPI>::B && ok) ? a.b[idx] : 0.0;
+    pp[t] = (EpiNeeds<EPI>::P2 && ok) ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx]) : 0.0;
+  }
+  // stage planes i0-1 .. i0+ni, batched so many loads are in flight per thread
+  const int total = (ni + 2) * TC::PSZ;
+  constexpr int U = 8;
+  for (int base = tid; base < total; base += TC::NT * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * TC::NT;
+      v[u] = 0.0;
+      if (e < total) {
+        const int p = e / TC::PSZ;
+        const int r = e - p * TC::PSZ;
+        const int hj = DIM == 3 ? r / TC::PW : 0;
+        const int hk = DIM == 3 ? r - hj * TC::PW : r;
+        const int gj = DIM == 3 ? j0 - 1 + hj : 0;
+        const int gk = k0 - 1 + hk;
+        const int ip = i0 - 1 + p;
+        if (gk <= g.n && gj <= g.n) {
+          const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
+          v[u] = stage_val<DIM, LOAD>(g, op, a, lin, ip, gj, gk);
+        }
       }
-      const uint32_t idx = DIM == 3 ? (uint32_t)i * g.ps + (uint32_t)j * g.s + k : (uint32_t)i * g.s + k;
-      epilogue<DIM, EPI>(a, idx, s_own, As, op.invd);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * TC::NT;
+      if (e < total) tile[e] = v[u];
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+#pragma unroll
+  for (int t = 0; t < TI; ++t) {
+    if (t >= ni) break;
+    double As = 0.0, s_own = 0.0;
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      const int di = off_comp(DIM, o, 0);
+      const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
+      const int dk = off_comp(DIM, o, DIM - 1);
+      const double sv = tile[(t + 1 + di) * TC::PSZ + (DIM == 3 ? (tj + 1 + dj) * TC::PW : 0) + tk + 1 + dk];
+      if (o == Traits<DIM>::CENTER) s_own = sv;
+      As = fma(op.w[o], sv, As);
+    }
+    epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, pb[t], pp[t]);
   }
 }
 

@@ -31,14 +31,18 @@ OPS = [("M", _lib.OP_M), ("K", _lib.OP_K), ("A", _lib.OP_A), ("VCYCLE", _lib.OP_
        ("SCHUR_TILDE_INV", _lib.OP_SCHUR_TILDE_INV), ("S_INV_APPROX", _lib.OP_S_INV_APPROX)]
 
 
-# tiled_min_n: 0 = default kernel choice (small grids use the one-thread-per-vertex
-# kernels), 2 = force the shared-memory tiled kernels on every level
-@pytest.fixture(scope="module", params=[(c, t) for c in golden_cases() for t in (0, 2)],
-                ids=lambda p: f"{p[0]}-tiled{p[1]}")
+# kernel-path modes: default choice; shared-memory tiled kernels forced on every
+# level (no single-CTA tail); one-thread-per-vertex kernels + the largest tail
+MODES = {"default": {}, "tiled": dict(tiled_min_n=2, tail_max_vertices=-1),
+         "tail": dict(tiled_min_n=-1, tail_max_vertices=1 << 30)}
+
+
+@pytest.fixture(scope="module", params=[(c, m) for c in golden_cases() for m in MODES],
+                ids=lambda p: f"{p[0]}-{p[1]}")
 def golden_ctx(request):
-    case, tiled = request.param
+    case, mode = request.param
     g = load_golden(case)
-    ctx = okg.SchurContext(golden_config(g), tiled_min_n=tiled)
+    ctx = okg.SchurContext(golden_config(g), **MODES[mode])
     yield g, ctx
     ctx.close()
 
@@ -318,12 +322,12 @@ KNOBS = [dict(cheby_iters=1, mg_cycles=1, richardson_steps=1), dict(mg_pre=1, mg
 
 
 @pytest.mark.parametrize("kw", KNOBS, ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()))
-@pytest.mark.parametrize("dim,n,tiled", [(2, 32, 0), (2, 32, 2), (3, 8, 2)])
-def test_solver_knobs_match_oracle(port_lib, kw, dim, n, tiled):
+@pytest.mark.parametrize("dim,n,mode", [(2, 32, "default"), (2, 32, "tiled"), (3, 8, "tiled"), (3, 8, "tail")])
+def test_solver_knobs_match_oracle(port_lib, kw, dim, n, mode):
     p = po.baseline_params(dim, n, kind="port", min_coarse_size=10, **kw)
     o = po.Oracle(p, "port")
     cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, min_coarse_size=10, **kw)
-    ctx = okg.SchurContext(cfg, tiled_min_n=tiled)
+    ctx = okg.SchurContext(cfg, **MODES[mode])
     assert ctx.level_sizes == [o.level_size(l) for l in range(o.levels)]
     u = okg.seeded_ic(ctx.n, 1, 0.0) + 0.2 * np.random.default_rng(1).uniform(-1, 1, ctx.n)
     ctx.linearize(u)
