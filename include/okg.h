@@ -63,7 +63,7 @@ typedef struct okg_params {
                                kernels; 0 = default (3D: 32, 2D: 128), < 0 = never */
   int32_t tail_max_vertices;/* multigrid levels (below the finest) with at most this many
                                vertices run as ONE single-CTA V-cycle kernel;
-                               0 = default (6000), < 0 = never */
+                               0 = default (1100), < 0 = never */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */

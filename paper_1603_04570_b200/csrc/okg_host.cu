@@ -495,6 +495,20 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
 }
 
 // ---- u-dependent blocks ---------------------------------------------------------
+template <int DIM, int MODE, int TI>
+static void tiled_c(okg_ctx* c, const CTArgs& t, Reduce rd) {
+  static bool attr = false;
+  const size_t smem = (size_t)CNeeds<MODE>::NOPS * (TI + 2) * TileCfg<DIM>::PSZ * sizeof(double);
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_tiled_c<DIM, MODE, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const Level& L0 = c->lv[0];
+  k_tiled_c<DIM, MODE, TI><<<L0.tl_blocks, TileCfg<DIM>::NT, smem, c->stream>>>(
+      L0.g, dev_op<DIM>(c->M), dev_op<DIM>(c->K), dev_op<DIM>(c->A), L0.tl, t, rd);
+  note(c);
+}
+
 template <int DIM, int MODE>
 static void capply(okg_ctx* c, const double* x, const double* v, const double* b, double* y, double s1,
                    Reduce rd = Reduce{nullptr, nullptr, nullptr}) {
@@ -508,6 +522,22 @@ static void capply(okg_ctx* c, const double* x, const double* v, const double* b
   a.n2 = c->N;
   a.s1 = s1;
   a.s2 = 0.0;
+  const Level& L0 = c->lv[0];
+  if (L0.tiled) {
+    CTArgs t;
+    t.x = x;
+    t.v = v;
+    t.b = b;
+    t.y = y;
+    t.coef = c->coef;
+    t.ldc = c->N;
+    t.n2 = c->N;
+    t.s1 = s1;
+    if (L0.tl.ichunk == 8) tiled_c<DIM, MODE, 8>(c, t, rd);
+    else if (L0.tl.ichunk == 4) tiled_c<DIM, MODE, 4>(c, t, rd);
+    else tiled_c<DIM, MODE, 2>(c, t, rd);
+    return;
+  }
   k_capply<DIM, MODE><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K),
                                                         dev_op<DIM>(c->A), a, rd);
   note(c);
@@ -963,7 +993,7 @@ static void build(okg_ctx* c) {
       L.res = dalloc(c, nl);
     }
     // single-CTA tail for the small levels (okg_tail.cuh)
-    const int64_t tmax = p.tail_max_vertices == 0 ? 6000 : p.tail_max_vertices;
+    const int64_t tmax = p.tail_max_vertices == 0 ? 1100 : p.tail_max_vertices;
     if (tmax > 0) {
       for (size_t l = 1; l < c->lv.size(); ++l)
         if ((int64_t)c->lv[l].g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL) {

@@ -648,3 +648,5 @@ __global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ 
 }
 
 }  // namespace okg
+
+#include "okg_tiled_c.cuh"

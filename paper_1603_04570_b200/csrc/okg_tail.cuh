@@ -58,13 +58,21 @@ __device__ __forceinline__ double tail_row(const TailLevel<DIM>& L, uint32_t idx
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(TAIL_NT) k_vcycle_tail(TailArgs<DIM> A) {
+__global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> Ap) {
   constexpr int NO = Traits<DIM>::NOFF;
   const int tid = threadIdx.x;
+  __shared__ TailArgs<DIM> A;
+  __shared__ double* cur[TAIL_MAXL];
+  __shared__ double* oth[TAIL_MAXL];
+  {  // word-wise copy of the level descriptors into shared memory
+    static_assert(sizeof(TailArgs<DIM>) % 8 == 0, "TailArgs must be 8-byte sized");
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&Ap);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&A);
+    for (int w = tid; w < (int)(sizeof(TailArgs<DIM>) / 8); w += TAIL_NT) dst[w] = src[w];
+  }
+  __syncthreads();
   const double om = A.omega;
   // down sweep: cur[l] holds the pre-smoothed iterate of level l
-  double* cur[TAIL_MAXL];
-  double* oth[TAIL_MAXL];
   for (int l = 0; l < A.nl - 1; ++l) {
     const TailLevel<DIM>& L = A.L[l];
     const double* rhs = l == 0 ? A.rhs : L.b;
@@ -118,8 +126,10 @@ __global__ void __launch_bounds__(TAIL_NT) k_vcycle_tail(TailArgs<DIM> A) {
       }
       C.b[i] = s;
     }
-    cur[l] = c;
-    oth[l] = o;
+    if (tid == 0) {
+      cur[l] = c;
+      oth[l] = o;
+    }
     __syncthreads();
   }
   // coarsest: x = A_c^{-1} b (warp per row)

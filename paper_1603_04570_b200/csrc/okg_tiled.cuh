@@ -241,3 +241,4 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
 }
 
 }  // namespace okg
+
