@@ -1,0 +1,345 @@
+// okg/okflow.hpp -- C++ host API of the B200 Newton linear solve, mirroring the
+// reference okflow interface for this path (same names, argument meaning and
+// exceptions), implemented over the C ABI of okg.h (libokg.so).
+//
+//   reference (namespace okflow)                      here (namespace okg)
+//   SolverConfig            params.hpp:14-117          SolverConfig
+//   State, IterationStats   model.hpp:25-42            State, IterationStats
+//   KrylovResult            krylov.hpp:21-28           KrylovResult
+//   LinearOperator          operator.hpp:16-37         LinearOperator (host vectors)
+//   make_schur_context      precond.hpp:126-181        make_schur_context -> SchurContext
+//   apply_block / jacobian_operator / block_preconditioner   precond.hpp:257-307
+//   gmres(jac, prec, b,...) krylov.hpp:44-152          gmres(ctx, b, ...)
+//   residual                model.hpp:121-148          residual
+//   newton_solve            model.hpp:165-215          newton_solve
+//   advance (minus energy)  model.hpp:218-227          advance
+//   errors.hpp:9-28 exception types                    same names, thrown from status codes
+//
+// The mesh and the operators M, K are implicit in the structured grid, so the
+// context is built from the SolverConfig alone; everything else keeps the
+// reference's signatures up to that.
+#pragma once
+
+#include <cmath>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../okg.h"
+
+namespace okg {
+
+using Vector = std::vector<double>;
+
+// ---- errors.hpp:9-28 ----------------------------------------------------------
+struct CannotCoarsen : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InconsistentState : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int status) {
+  if (status == OKG_OK) return;
+  char buf[1024];
+  okg_last_error(buf, sizeof buf);
+  const std::string msg(buf);
+  switch (status) {
+    case OKG_EINVAL: throw std::invalid_argument(msg);
+    case OKG_ENUMERICAL: throw NumericalError(msg);
+    case OKG_ECONFIG: throw ConfigError(msg);
+    case OKG_EINCONSISTENT: throw InconsistentState(msg);
+    case OKG_ECOARSEN: throw CannotCoarsen(msg);
+    case OKG_ENOMEM: throw std::bad_alloc();
+    default: throw CudaError(msg);
+  }
+}
+
+// ---- params.hpp:14-117 ---------------------------------------------------------
+struct SolverConfig {
+  double eps = 0.02, sigma = 100.0, m = 0.4, theta = 0.5;
+  double dt = 4.0e-4;
+  int n_steps = 25;
+  int dim = 2, n = 64;
+  double newton_tol = 1e-8;
+  int newton_maxit = 20;
+  double gmres_tol = 1e-6;
+  int gmres_maxit = 200, gmres_restart = 0;
+  int cheby_iters = 10;
+  std::string cheby_precond = "jacobi";
+  int richardson_steps = 2, mg_cycles = 5, mg_pre = 2, mg_post = 2;
+  double mg_omega = 2.0 / 3.0;
+  int min_coarse_size = 500;
+  int threads = 1;
+  long max_dofs = 2000000;
+  int device = 0;
+
+  long num_vertices() const {
+    long s = static_cast<long>(n) + 1, v = s * s;
+    return dim == 3 ? v * s : v;
+  }
+  okg_params to_params(double shat_perturb = 0.0) const {
+    okg_params p;
+    okg_default_params(&p);
+    p.dim = dim;
+    p.n = n;
+    p.eps = eps;
+    p.sigma = sigma;
+    p.m = m;
+    p.theta = theta;
+    p.dt = dt;
+    p.newton_tol = newton_tol;
+    p.newton_maxit = newton_maxit;
+    p.gmres_tol = gmres_tol;
+    p.gmres_maxit = gmres_maxit;
+    p.gmres_restart = gmres_restart;
+    p.cheby_iters = cheby_iters;
+    p.richardson_steps = richardson_steps;
+    p.mg_cycles = mg_cycles;
+    p.mg_pre = mg_pre;
+    p.mg_post = mg_post;
+    p.mg_omega = mg_omega;
+    p.min_coarse_size = min_coarse_size;
+    p.max_dofs = max_dofs;
+    p.shat_perturb = shat_perturb;
+    p.device = device;
+    return p;
+  }
+  void validate() const {  // SolverConfig::validate
+    if (cheby_precond != "jacobi" && cheby_precond != "ssor")
+      throw ConfigError("config: cheby_precond must be 'jacobi' or 'ssor'");
+    if (n_steps < 0) throw ConfigError("config: n_steps must be nonnegative");
+    if (threads < 1) throw ConfigError("config: threads must be at least 1");
+    const okg_params p = to_params();
+    check(okg_validate_params(&p));
+  }
+};
+
+inline double compute_c(double dt, double theta, double sigma) {  // precond.hpp:31-38
+  if (!(dt > 0.0)) throw std::invalid_argument("compute_c: dt must be positive");
+  if (!(theta > 0.0) || theta > 1.0) throw std::invalid_argument("compute_c: theta must lie in (0, 1]");
+  if (sigma < 0.0) throw std::invalid_argument("compute_c: sigma must be nonnegative");
+  return dt * theta / (1.0 + dt * theta * sigma);
+}
+
+// ---- model.hpp:25-42, krylov.hpp:21-28 ------------------------------------------
+struct State {
+  Vector u, w;
+  double t = 0.0;
+  int step = 0;
+};
+
+struct IterationStats {
+  int step = 0;
+  double t = 0.0;
+  int newton_iters = 0;
+  std::vector<int> gmres_iters;
+  double residual_norm = 0.0;
+  double mass = 0.0;
+  double energy = NAN;  // energy diagnostic: out of scope on the GPU path
+  double seconds = 0.0;
+  bool converged = true;
+};
+
+struct KrylovResult {
+  Vector x;
+  int iterations = 0;
+  std::vector<double> residual_norms;
+  bool converged = false;
+  bool stagnated = false;
+  double final_residual = 0.0;
+};
+
+// RAII device buffer (host-API convenience)
+class DeviceVector {
+ public:
+  DeviceVector(size_t n, int device) : n_(n) { check(okg_device_alloc(device, (n ? n : 1) * sizeof(double), &p_)); }
+  DeviceVector(const Vector& v, int device) : DeviceVector(v.size(), device) {
+    check(okg_memcpy_h2d(p_, v.data(), v.size() * sizeof(double)));
+  }
+  ~DeviceVector() {
+    if (p_) okg_device_free(p_);
+  }
+  DeviceVector(const DeviceVector&) = delete;
+  DeviceVector& operator=(const DeviceVector&) = delete;
+  Vector host() const {
+    Vector v(n_);
+    check(okg_memcpy_d2h(v.data(), p_, n_ * sizeof(double)));
+    return v;
+  }
+  double* get() const { return static_cast<double*>(p_); }
+
+ private:
+  size_t n_;
+  void* p_ = nullptr;
+};
+
+// ---- precond.hpp:56-181: the context (plus the device workspace) ------------------
+class SchurContext {
+ public:
+  explicit SchurContext(const SolverConfig& cfg, double shat_perturb = 0.0) : cfg_(cfg) {
+    const okg_params p = cfg.to_params(shat_perturb);
+    check(okg_create(&p, &h_));
+    check(okg_get_info(h_, &info_));
+  }
+  ~SchurContext() {
+    if (h_) okg_destroy(h_);
+  }
+  SchurContext(const SchurContext&) = delete;
+  SchurContext& operator=(const SchurContext&) = delete;
+  SchurContext(SchurContext&& o) noexcept : cfg_(o.cfg_), h_(o.h_), info_(o.info_), me_set_(o.me_set_) {
+    o.h_ = nullptr;
+  }
+
+  int rows() const { return static_cast<int>(info_.num_vertices); }
+  double c() const { return info_.c; }
+  double sqrt_c() const { return info_.sqrt_c; }
+  double a_coeff() const { return info_.a_coeff; }
+  double dt_theta() const { return info_.dt_theta; }
+  double lambda_lo() const { return info_.lambda_lo; }
+  double lambda_hi() const { return info_.lambda_hi; }
+  int levels() const { return info_.levels; }
+  const SolverConfig& config() const { return cfg_; }
+  okg_ctx* handle() const { return h_; }
+  int device() const { return cfg_.device; }
+
+  // ctx.Me = assemble_coefficient_mass(mesh, u)   (model.hpp:184-185)
+  void set_linearization(const Vector& u) {
+    DeviceVector d(u, device());
+    check(okg_linearize(h_, d.get()));
+    me_set_ = true;
+  }
+  void clear_linearization() {
+    check(okg_clear_linearization(h_));
+    me_set_ = false;
+  }
+  Vector apply(int kind, const Vector& x, size_t out_size, int level = 0) const {
+    DeviceVector dx(x, device()), dy(out_size, device());
+    check(okg_apply(h_, kind, level, dx.get(), dy.get()));
+    return dy.host();
+  }
+
+ private:
+  SolverConfig cfg_;
+  okg_ctx* h_ = nullptr;
+  okg_info info_{};
+  bool me_set_ = false;
+};
+
+inline SchurContext make_schur_context(const SolverConfig& cfg, double shat_perturb = 0.0) {
+  return SchurContext(cfg, shat_perturb);
+}
+
+// ---- operator.hpp:16-37 ------------------------------------------------------------
+struct LinearOperator {
+  int n = 0;
+  int n_in = 0;
+  std::function<void(const Vector&, Vector&)> apply_fn;
+  std::string label;
+  void apply(const Vector& x, Vector& y) const {
+    if (static_cast<int>(x.size()) != cols())
+      throw std::invalid_argument("operator '" + label + "': input dimension mismatch");
+    apply_fn(x, y);
+  }
+  Vector operator()(const Vector& x) const {
+    Vector y;
+    apply(x, y);
+    return y;
+  }
+  int rows() const { return n; }
+  int cols() const { return n_in > 0 ? n_in : n; }
+};
+
+// ---- precond.hpp:257-307 -------------------------------------------------------------
+inline Vector apply_block(const SchurContext& ctx, const Vector& r) {
+  const int n = ctx.rows();
+  if (static_cast<int>(r.size()) != 2 * n) throw std::invalid_argument("block preconditioner: stacked size mismatch");
+  return ctx.apply(OKG_OP_BLOCK, r, 2 * static_cast<size_t>(n));
+}
+
+inline LinearOperator jacobian_operator(const SchurContext& ctx) {
+  const int n = ctx.rows();
+  return {2 * n, 2 * n,
+          [&ctx, n](const Vector& x, Vector& y) { y = ctx.apply(OKG_OP_JACOBIAN, x, 2 * static_cast<size_t>(n)); },
+          "coupled-jacobian"};
+}
+
+inline LinearOperator block_preconditioner(const SchurContext& ctx) {
+  const int n = ctx.rows();
+  return {2 * n, 2 * n, [&ctx](const Vector& r, Vector& y) { y = apply_block(ctx, r); }, "block-triangular"};
+}
+
+// gmres(jacobian_operator(ctx), block_preconditioner(ctx), b, ...)  (krylov.hpp:44-152),
+// run entirely on the device.
+inline KrylovResult gmres(const SchurContext& ctx, const Vector& b, double rel_tol, int max_iter, int restart = 0) {
+  const int n = ctx.rows();
+  if (static_cast<int>(b.size()) != 2 * n) throw std::invalid_argument("gmres: rhs dimension mismatch");
+  DeviceVector db(b, ctx.device()), dx(b.size(), ctx.device());
+  okg_krylov_stats ks;
+  check(okg_gmres(ctx.handle(), db.get(), dx.get(), rel_tol, max_iter, restart, &ks));
+  KrylovResult r;
+  r.x = dx.host();
+  r.iterations = ks.iterations;
+  r.converged = ks.converged != 0;
+  r.stagnated = ks.stagnated != 0;
+  r.final_residual = ks.final_residual;
+  for (int i = 0; i < ks.n_residual_norms && i < 512; ++i) r.residual_norms.push_back(ks.residual_norms[i]);
+  return r;
+}
+
+// ---- model.hpp:121-227 ------------------------------------------------------------------
+inline std::pair<Vector, Vector> residual(const State& next, const State& old, const SchurContext& ctx) {
+  const size_t n = static_cast<size_t>(ctx.rows());
+  if (next.u.size() != old.u.size() || next.w.size() != old.w.size() || next.u.size() != n)
+    throw std::invalid_argument("residual: states do not match the mesh");
+  DeviceVector un(next.u, ctx.device()), wn(next.w, ctx.device()), uo(old.u, ctx.device()),
+      wo(old.w, ctx.device()), r1(n, ctx.device()), r2(n, ctx.device());
+  check(okg_residual(ctx.handle(), un.get(), wn.get(), uo.get(), wo.get(), r1.get(), r2.get()));
+  return {r1.host(), r2.host()};
+}
+
+inline std::pair<State, IterationStats> newton_solve(const State& old, SchurContext& ctx,
+                                                     const SolverConfig& /*cfg: ctx holds it*/) {
+  const size_t n = static_cast<size_t>(ctx.rows());
+  if (old.u.size() != n || old.w.size() != n) throw std::invalid_argument("residual: states do not match the mesh");
+  State next;
+  next.u.resize(n);
+  next.w.resize(n);
+  check(okg_set_state(ctx.handle(), old.u.data(), old.w.data(), old.t, old.step));
+  okg_step_stats st;
+  check(okg_newton_step(ctx.handle(), &st));
+  check(okg_get_state(ctx.handle(), next.u.data(), next.w.data(), &next.t, &next.step));
+  IterationStats s;
+  s.step = st.step;
+  s.t = st.t;
+  s.newton_iters = st.newton_iters;
+  for (int i = 0; i < st.newton_iters && i < OKG_MAX_NEWTON; ++i) s.gmres_iters.push_back(st.gmres_iters[i]);
+  s.residual_norm = st.residual_norm;
+  s.seconds = st.seconds;
+  s.converged = st.converged != 0;
+  return {std::move(next), std::move(s)};
+}
+
+inline std::pair<State, IterationStats> advance(const State& state, SchurContext& ctx, const SolverConfig& cfg) {
+  auto res = newton_solve(state, ctx, cfg);
+  // total_mass = b^T u with b = M 1 (model.hpp:46-48)
+  const Vector ones(static_cast<size_t>(ctx.rows()), 1.0);
+  const Vector b = ctx.apply(OKG_OP_M, ones, ones.size());
+  double mass = 0.0;
+  for (size_t i = 0; i < b.size(); ++i) mass += b[i] * res.first.u[i];
+  res.second.mass = mass;
+  return res;
+}
+
+}  // namespace okg

@@ -1,0 +1,30 @@
+"""The C++ host API (include/okg/okflow.hpp) on a GPU: tests/cpp/test_okflow_api.cpp."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BIN = os.path.join(ROOT, "tests", "cpp", "test_okflow_api")
+SRC = BIN + ".cpp"
+
+
+def build_cpp():
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), SRC, "-o", BIN,
+                           "-L" + os.path.join(ROOT, "paper_1603_04570_b200"), "-lokg",
+                           "-Wl,-rpath,$ORIGIN/../../paper_1603_04570_b200"])
+
+
+def test_cpp_api_compiles():
+    build_cpp()
+    assert os.path.exists(BIN)
+
+
+@pytest.mark.gpu
+def test_cpp_api_on_gpu():
+    if not os.path.exists(BIN):
+        build_cpp()
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "all C++ host-API checks passed" in out.stdout
