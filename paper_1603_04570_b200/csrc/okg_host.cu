@@ -255,6 +255,7 @@ static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& 
   const size_t smem = (size_t)(TI + 2) * TileCfg<DIM>::PSZ * sizeof(double);
   if (!attr) {
     CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
   k_tiled<DIM, LOAD, EPI, TI><<<L.tl_blocks, TileCfg<DIM>::NT, smem, c->stream>>>(L.g, dev_op<DIM>(op), L.tl, a);
@@ -288,8 +289,9 @@ static void make_tiling(okg_ctx* c, Level& L) {
   t.ktiles = (n - 1 + TC::TK - 1) / TC::TK;
   t.jtiles = DIM == 3 ? (n - 1 + TC::TJ - 1) / TC::TJ : 1;
   const int base = t.ktiles * t.jtiles;
-  // vertices per thread along x (TI): as deep as possible while keeping >= ~4 CTAs per SM
-  int ichunk = 8;
+  // vertices per thread along x (TI): 3D 4 (register budget for 6 CTAs/SM), 2D 8;
+  // smaller when the level is too small to give each SM a few CTAs
+  int ichunk = DIM == 3 ? 4 : 8;
   while (ichunk > 2 && base * ((n - 1 + ichunk - 1) / ichunk) < 148 * 4) ichunk /= 2;
   const int nchunks = (n - 1 + ichunk - 1) / ichunk;
   t.ichunk = ichunk;
@@ -501,6 +503,7 @@ static void tiled_c(okg_ctx* c, const CTArgs& t, Reduce rd) {
   const size_t smem = (size_t)CNeeds<MODE>::NOPS * (TI + 2) * TileCfg<DIM>::PSZ * sizeof(double);
   if (!attr) {
     CK(cudaFuncSetAttribute(k_tiled_c<DIM, MODE, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_tiled_c<DIM, MODE, TI>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
   const Level& L0 = c->lv[0];
