@@ -64,6 +64,7 @@ typedef struct okg_params {
   int32_t tail_max_vertices;/* multigrid levels (below the finest) with at most this many
                                vertices run as ONE single-CTA V-cycle kernel;
                                0 = default (1100), < 0 = never */
+  int32_t disable_pdl;      /* 1: launch without programmatic dependent launch */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */

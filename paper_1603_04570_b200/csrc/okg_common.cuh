@@ -19,6 +19,20 @@
 
 namespace okg {
 
+// Programmatic dependent launch (Hopper/Blackwell): every kernel is launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, waits for its
+// predecessor grid's completion (and memory) before touching global memory,
+// and immediately lets its own dependent grid be scheduled, so launch latency
+// and CTA ramp-up overlap the predecessor's tail.  griddepcontrol.wait is a
+// no-op for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define PDL_ENTRY() \
+  do {              \
+    pdl_wait();     \
+    pdl_trigger();  \
+  } while (0)
+
 template <int DIM>
 struct Traits;
 template <>

@@ -160,6 +160,23 @@ static void note(okg_ctx* c) {
   if (e != cudaSuccess) THROW(OKG_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
 }
 
+// every kernel goes through here: PDL attribute (okg_common.cuh) + launch count
+template <class... KArgs, class... Args>
+static void launch(okg_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = c->p.disable_pdl ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) THROW(OKG_ECUDA, "cudaLaunchKernelEx: %s", cudaGetErrorString(e));
+}
+
 static unsigned nblk(size_t n) { return static_cast<unsigned>((n + BS - 1) / BS); }
 static unsigned vblk(size_t n) { return static_cast<unsigned>(std::min<size_t>((n + BS - 1) / BS, 148 * 8)); }
 
@@ -233,17 +250,17 @@ static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const
                      double* y, double* acc, double omega = 0.0) {
   const Op<DIM> o = dev_op<DIM>(op);
   switch (epi) {
-    case EPI_APPLY: k_op<DIM, EPI_APPLY><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega); break;
-    case EPI_RESID: k_op<DIM, EPI_RESID><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega); break;
-    case EPI_JACOBI: k_op<DIM, EPI_JACOBI><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega); break;
+    case EPI_APPLY: launch(c, k_op<DIM, EPI_APPLY>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega); break;
+    case EPI_RESID: launch(c, k_op<DIM, EPI_RESID>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega); break;
+    case EPI_JACOBI: launch(c, k_op<DIM, EPI_JACOBI>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega); break;
     case EPI_JACOBI_SET:
-      k_op<DIM, EPI_JACOBI_SET><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega);
+      launch(c, k_op<DIM, EPI_JACOBI_SET>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega);
       break;
     case EPI_JACOBI_ACC:
-      k_op<DIM, EPI_JACOBI_ACC><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega);
+      launch(c, k_op<DIM, EPI_JACOBI_ACC>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega);
       break;
     case EPI_SCALE_APPLY:
-      k_op<DIM, EPI_SCALE_APPLY><<<nblk(g.N), BS, 0, c->stream>>>(g, o, x, b, y, acc, omega);
+      launch(c, k_op<DIM, EPI_SCALE_APPLY>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega);
       break;
   }
   note(c);
@@ -258,7 +275,7 @@ static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& 
     CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr = true;
   }
-  k_tiled<DIM, LOAD, EPI, TI><<<L.tl_blocks, TileCfg<DIM>::NT, smem, c->stream>>>(L.g, dev_op<DIM>(op), L.tl, a);
+  launch(c, k_tiled<DIM, LOAD, EPI, TI>, L.tl_blocks, TileCfg<DIM>::NT, smem, L.g, dev_op<DIM>(op), L.tl, a);
   note(c);
 }
 
@@ -318,11 +335,11 @@ static void make_tiling(okg_ctx* c, Level& L) {
 }
 
 static void axpy(okg_ctx* c, double a, const double* x, double* y, size_t n) {
-  k_axpy<<<vblk(n), BS, 0, c->stream>>>(a, x, y, n);
+  launch(c, k_axpy, vblk(n), BS, 0, a, x, y, n);
   note(c);
 }
 static void scale(okg_ctx* c, double s, const double* x, double* y, size_t n) {
-  k_scale<<<vblk(n), BS, 0, c->stream>>>(s, x, y, n);
+  launch(c, k_scale, vblk(n), BS, 0, s, x, y, n);
   note(c);
 }
 static void copy(okg_ctx* c, const double* x, double* y, size_t n) {
@@ -332,7 +349,7 @@ static void copy(okg_ctx* c, const double* x, double* y, size_t n) {
 // ---- multigrid (multigrid.hpp:97-149) --------------------------------------
 template <int DIM>
 static void coarse_solve(okg_ctx* c, const double* b, double* y) {
-  k_coarse_solve<<<(c->nc + BS / 32 - 1) / (BS / 32), BS, 0, c->stream>>>(c->nc, c->Ainv, b, y);
+  launch(c, k_coarse_solve, (c->nc + BS / 32 - 1) / (BS / 32), BS, 0, c->nc, c->Ainv, b, y);
   note(c);
 }
 
@@ -359,7 +376,7 @@ static void run_tail(okg_ctx* c, int l0, const double* rhs, double* out) {
   A.out = out;
   A.Ainv = c->Ainv;
   A.nc = c->nc;
-  k_vcycle_tail<DIM><<<1, TAIL_NT, 0, c->stream>>>(A);
+  launch(c, k_vcycle_tail<DIM>, 1, TAIL_NT, 0, A);
   note(c);
 }
 
@@ -391,7 +408,7 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   } else if (pre >= 2) {
     if (L.tiled) tiled<DIM, L_JAC0, T_JACOBI>(c, L, L.shat, targs(rhs, rhs, cur, nullptr, om));
     else {
-      k_pre2<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
+      launch(c, k_pre2<DIM>, nblk(L.g.N), BS, 0, L.g, op, rhs, cur, om);
       note(c);
     }
     for (int s = 2; s < pre; ++s) {
@@ -400,19 +417,19 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
       std::swap(cur, oth);
     }
   } else {
-    k_jacobi0<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, op, rhs, cur, om);
+    launch(c, k_jacobi0<DIM>, nblk(L.g.N), BS, 0, L.g, op, rhs, cur, om);
     note(c);
   }
   // ---- residual, restriction, coarse correction (multigrid.hpp:106-110)
   if (L.tiled) tiled<DIM, L_PLAIN, T_RESID>(c, L, L.shat, targs(cur, rhs, L.res, nullptr, 0.0));
   else op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
   Level& C = c->lv[l + 1];
-  k_restrict<DIM><<<nblk(C.g.N), BS, 0, c->stream>>>(L.g, C.g, L.res, C.b);
+  launch(c, k_restrict<DIM>, nblk(C.g.N), BS, 0, L.g, C.g, L.res, C.b);
   note(c);
   mg_level<DIM>(c, l + 1, C.b, C.x, false);
   // ---- prolongation + post-smoothing (multigrid.hpp:111-115)
   if (post == 0 || !L.tiled) {
-    k_prolong_add<DIM><<<nblk(L.g.N), BS, 0, c->stream>>>(L.g, C.g, C.x, cur);
+    launch(c, k_prolong_add<DIM>, nblk(L.g.N), BS, 0, L.g, C.g, C.x, cur);
     note(c);
   }
   for (int s = 0; s < post; ++s) {
@@ -471,7 +488,7 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
   const int k = c->p.cheby_iters;
   double* dcur = c->cd0;
   double* dnxt = c->cd1;
-  k_cheb_first<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, o, b, dcur, c->cheb_inv_theta);
+  launch(c, k_cheb_first<DIM>, nblk(g.N), BS, 0, g, o, b, dcur, c->cheb_inv_theta);
   note(c);
   if (k == 1) {
     copy(c, dcur, x, g.N);
@@ -488,7 +505,7 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
       a.last = last;
       tiled<DIM, L_PLAIN, T_CHEB>(c, c->lv[0], A, a);
     } else {
-      k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
+      launch(c, k_cheb_step<DIM>, nblk(g.N), BS, 0, g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
                                                         c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last);
       note(c);
     }
@@ -507,7 +524,7 @@ static void tiled_c(okg_ctx* c, const CTArgs& t, Reduce rd) {
     attr = true;
   }
   const Level& L0 = c->lv[0];
-  k_tiled_c<DIM, MODE, TI><<<L0.tl_blocks, TileCfg<DIM>::NT, smem, c->stream>>>(
+  launch(c, k_tiled_c<DIM, MODE, TI>, L0.tl_blocks, TileCfg<DIM>::NT, smem, 
       L0.g, dev_op<DIM>(c->M), dev_op<DIM>(c->K), dev_op<DIM>(c->A), L0.tl, t, rd);
   note(c);
 }
@@ -541,7 +558,7 @@ static void capply(okg_ctx* c, const double* x, const double* v, const double* b
     else tiled_c<DIM, MODE, 2>(c, t, rd);
     return;
   }
-  k_capply<DIM, MODE><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K),
+  launch(c, k_capply<DIM, MODE>, nblk(c->N), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K),
                                                         dev_op<DIM>(c->A), a, rd);
   note(c);
 }
@@ -658,7 +675,7 @@ static double residual(okg_ctx* c, const double* un, const double* wn, const dou
   a.eps2 = c->p.eps * c->p.eps;
   a.b_int = c->b_int;
   a.b_tab = c->b_tab;
-  k_residual<DIM><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K), c->nl, a,
+  launch(c, k_residual<DIM>, nblk(c->N), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K), c->nl, a,
                                                    red(c, R_RES));
   note(c);
   sync_read(c, R_RES, 2);
@@ -669,7 +686,7 @@ static double residual(okg_ctx* c, const double* un, const double* wn, const dou
 
 template <int DIM>
 static void linearize(okg_ctx* c, const double* u) {
-  k_linearize<DIM><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, dev_op<DIM>(c->K), c->nl, c->p.eps * c->p.eps, u,
+  launch(c, k_linearize<DIM>, nblk(c->N), BS, 0, c->fine, dev_op<DIM>(c->K), c->nl, c->p.eps * c->p.eps, u,
                                                     c->coef, c->N);
   note(c);
   c->have_lin = true;
@@ -685,13 +702,13 @@ static void givens(double cs, double sn, double& a, double& b) {
 template <int NVB>
 static void arnoldi_ortho(okg_ctx* c, int nv) {
   const size_t n2 = c->N2;
-  k_arnoldi_dot<NVB><<<vblk(n2), BS, 0, c->stream>>>(nv, c->pw, c->V, n2, n2, red(c, R_H));
+  launch(c, k_arnoldi_dot<NVB>, vblk(n2), BS, 0, nv, c->pw, c->V, n2, n2, red(c, R_H));
   note(c);
   // put ||w||^2 after the h values at a fixed slot
-  k_arnoldi_update<NVB, 0><<<vblk(n2), BS, 0, c->stream>>>(nv, c->pw, c->V, n2, n2, c->dred + R_H, c->gt,
+  launch(c, k_arnoldi_update<NVB, 0>, vblk(n2), BS, 0, nv, c->pw, c->V, n2, n2, c->dred + R_H, c->gt,
                                                            red(c, R_C));
   note(c);
-  k_arnoldi_update<NVB, 1><<<vblk(n2), BS, 0, c->stream>>>(nv, c->gt, c->V, n2, n2, c->dred + R_C, c->pw,
+  launch(c, k_arnoldi_update<NVB, 1>, vblk(n2), BS, 0, nv, c->gt, c->V, n2, n2, c->dred + R_C, c->pw,
                                                            red(c, R_NRM));
   note(c);
 }
@@ -704,7 +721,7 @@ static void arnoldi_ortho_chunked(okg_ctx* c, int nv, std::vector<double>& hsum,
     std::vector<double> hh(nv, 0.0);
     for (int q0 = 0; q0 < nv; q0 += 32) {
       const int cnt = std::min(32, nv - q0);
-      k_arnoldi_dot<32><<<vblk(n2), BS, 0, c->stream>>>(cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2, red(c, R_H));
+      launch(c, k_arnoldi_dot<32>, vblk(n2), BS, 0, cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2, red(c, R_H));
       note(c);
       sync_read(c, R_H, 33);
       for (int q = 0; q < cnt; ++q) hh[q0 + q] = c->hred[R_H + q];
@@ -713,7 +730,7 @@ static void arnoldi_ortho_chunked(okg_ctx* c, int nv, std::vector<double>& hsum,
     for (int q0 = 0; q0 < nv; q0 += 32) {
       const int cnt = std::min(32, nv - q0);
       CK(cudaMemcpyAsync(c->dred + R_C, hh.data() + q0, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      k_arnoldi_update<32, 1><<<vblk(n2), BS, 0, c->stream>>>(cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2,
+      launch(c, k_arnoldi_update<32, 1>, vblk(n2), BS, 0, cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2,
                                                              c->dred + R_C, c->gt, red(c, R_NRM));
       note(c);
       copy(c, c->gt, c->pw, n2);
@@ -738,7 +755,7 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
   CK(cudaMemsetAsync(x, 0, n2 * sizeof(double), c->stream));
   double nb2 = norm_b_sq;
   if (nb2 < 0.0) {
-    k_dot<<<vblk(n2), BS, 0, c->stream>>>(b, b, n2, red(c, R_DOT));
+    launch(c, k_dot, vblk(n2), BS, 0, b, b, n2, red(c, R_DOT));
     note(c);
     sync_read(c, R_DOT, 1);
     nb2 = c->hred[R_DOT];
@@ -760,7 +777,7 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
   std::vector<double> cs, sn, g, hsum;
   while (st->iterations < max_iter) {
     // V0 = r / beta
-    k_scale<<<vblk(n2), BS, 0, c->stream>>>(1.0 / beta, r, c->V, n2);
+    launch(c, k_scale, vblk(n2), BS, 0, 1.0 / beta, r, c->V, n2);
     note(c);
     copy(c, c->V, c->pin, n2);
     H.clear();
@@ -780,7 +797,7 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
         else if (nv <= 16) arnoldi_ortho<16>(c, nv);
         else arnoldi_ortho<32>(c, nv);
         // V_{j+1} = w / ||w||  (speculative; unused on exit)
-        k_normalize<<<vblk(n2), BS, 0, c->stream>>>(c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
+        launch(c, k_normalize, vblk(n2), BS, 0, c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
                                                      n2);
         note(c);
         const int nvb = nv <= 4 ? 4 : nv <= 8 ? 8 : nv <= 16 ? 16 : 32;
@@ -794,7 +811,7 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
         arnoldi_ortho_chunked(c, nv, hsum, ww);
         for (int q = 0; q < nv; ++q) h[q] = hsum[q];
         arnoldi_norm = std::sqrt(c->hred[R_NRM]);
-        k_normalize<<<vblk(n2), BS, 0, c->stream>>>(c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
+        launch(c, k_normalize, vblk(n2), BS, 0, c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
                                                      n2);
         note(c);
       }
@@ -835,10 +852,10 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
       const int cnt = std::min(32, j - q0);
       for (int q = 0; q < 32; ++q) yc.c[q] = q < cnt ? y[q0 + q] : 0.0;
       if (q0 == 0) {
-        k_combine<<<vblk(n2), BS, 0, c->stream>>>(std::max(cnt, 0), yc, c->V, n2, n2, c->pin);
+        launch(c, k_combine, vblk(n2), BS, 0, std::max(cnt, 0), yc, c->V, n2, n2, c->pin);
         note(c);
       } else {
-        k_combine<<<vblk(n2), BS, 0, c->stream>>>(cnt, yc, c->V + (size_t)q0 * n2, n2, n2, c->gt);
+        launch(c, k_combine, vblk(n2), BS, 0, cnt, yc, c->V + (size_t)q0 * n2, n2, n2, c->gt);
         note(c);
         axpy(c, 1.0, c->gt, c->pin, n2);
       }
@@ -875,7 +892,7 @@ static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
   for (auto& e : hv) e = dist(rng);
   std::vector<double*> Vv;
   auto dot = [&](const double* a, const double* b) {
-    k_dot<<<vblk(n), BS, 0, c->stream>>>(a, b, n, red(c, R_DOT));
+    launch(c, k_dot, vblk(n), BS, 0, a, b, n, red(c, R_DOT));
     note(c);
     sync_read(c, R_DOT, 1);
     return c->hred[R_DOT];
@@ -1142,7 +1159,7 @@ static void newton_step_impl(okg_ctx* c, okg_step_stats* stats) {
     if (st.newton_iters < OKG_MAX_NEWTON) st.gmres_iters[st.newton_iters] = ks.iterations;
     // require_finite(lin.x) (model.hpp:196)
     CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
-    k_check_finite<<<vblk(c->N2), BS, 0, c->stream>>>(c->gx, c->N2, c->dflag);
+    launch(c, k_check_finite, vblk(c->N2), BS, 0, c->gx, c->N2, c->dflag);
     note(c);
     int flag = 0;
     CK(cudaMemcpyAsync(&flag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -1186,12 +1203,12 @@ static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double*
     case OKG_OP_PROLONG:
       if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
       CK(cudaMemsetAsync(y, 0, c->lv[level].g.N * sizeof(double), c->stream));
-      k_prolong_add<DIM><<<nblk(c->lv[level].g.N), BS, 0, c->stream>>>(c->lv[level].g, c->lv[level + 1].g, x, y);
+      launch(c, k_prolong_add<DIM>, nblk(c->lv[level].g.N), BS, 0, c->lv[level].g, c->lv[level + 1].g, x, y);
       note(c);
       break;
     case OKG_OP_RESTRICT:
       if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
-      k_restrict<DIM><<<nblk(c->lv[level + 1].g.N), BS, 0, c->stream>>>(c->lv[level].g, c->lv[level + 1].g, x, y);
+      launch(c, k_restrict<DIM>, nblk(c->lv[level + 1].g.N), BS, 0, c->lv[level].g, c->lv[level + 1].g, x, y);
       note(c);
       break;
     case OKG_OP_VCYCLE: mg_level<DIM>(c, 0, x, y, false); break;
@@ -1224,7 +1241,7 @@ static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double*
       jacobian<DIM>(c, x, y);
       break;
     case OKG_OP_NONLINEAR:
-      k_nonlinear<DIM><<<nblk(c->N), BS, 0, c->stream>>>(c->fine, c->nl, x, y);
+      launch(c, k_nonlinear<DIM>, nblk(c->N), BS, 0, c->fine, c->nl, x, y);
       note(c);
       break;
     case OKG_OP_COARSE_SOLVE: coarse_solve<DIM>(c, x, y); break;
@@ -1550,7 +1567,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
   const double B = 8.0;
   // operands: reuse workspace vectors (contents are finite)
   double *x = c->cd0, *b = c->cd1, *y = c->cr, *z = c->kv;
-  auto launch = [&]() {
+  auto run_once = [&]() {
     const bool T = L0.tiled;
     switch (which) {
       case OKG_KT_SMOOTH:
@@ -1564,7 +1581,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
       case OKG_KT_PRE2:
         if (T) tiled<DIM, L_JAC0, T_JACOBI>(c, L0, L0.shat, targs(b, b, y, nullptr, om));
         else {
-          k_pre2<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(L0.shat), b, y, om);
+          launch(c, k_pre2<DIM>, nblk(g.N), BS, 0, g, dev_op<DIM>(L0.shat), b, y, om);
           note(c);
         }
         break;
@@ -1581,14 +1598,14 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
           a.c2 = c->cheb_c2[0];
           tiled<DIM, L_PLAIN, T_CHEB>(c, L0, c->A, a);
         } else {
-          k_cheb_step<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, dev_op<DIM>(c->A), x, b, y, c->zz, c->rr, z,
+          launch(c, k_cheb_step<DIM>, nblk(g.N), BS, 0, g, dev_op<DIM>(c->A), x, b, y, c->zz, c->rr, z,
                                                             c->cheb_c1[0], c->cheb_c2[0], 0);
           note(c);
         }
         break;
       case OKG_KT_JACOBIAN: jacobian<DIM>(c, c->pz, c->pw); break;
       case OKG_KT_RESTRICT:
-        k_restrict<DIM><<<nblk(c->lv[1].g.N), BS, 0, c->stream>>>(g, c->lv[1].g, x, c->lv[1].b);
+        launch(c, k_restrict<DIM>, nblk(c->lv[1].g.N), BS, 0, g, c->lv[1].g, x, c->lv[1].b);
         note(c);
         break;
       case OKG_KT_PROLONG:
@@ -1598,7 +1615,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
           a.gc = c->lv[1].g;
           tiled<DIM, L_PROLONG, T_JACOBI>(c, L0, L0.shat, a);
         } else {
-          k_prolong_add<DIM><<<nblk(g.N), BS, 0, c->stream>>>(g, c->lv[1].g, c->lv[1].x, y);
+          launch(c, k_prolong_add<DIM>, nblk(g.N), BS, 0, g, c->lv[1].g, c->lv[1].x, y);
           note(c);
         }
         break;
@@ -1619,12 +1636,12 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
     case OKG_KT_PROLONG: *bytes = (L0.tiled ? 3 * N + Nc : 2 * N + Nc) * B; break;
   }
   bool had_lin = c->have_lin;
-  for (int i = 0; i < 3; ++i) launch();
+  for (int i = 0; i < 3; ++i) run_once();
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
-  for (int i = 0; i < reps; ++i) launch();
+  for (int i = 0; i < reps; ++i) run_once();
   CK(cudaEventRecord(e1, c->stream));
   CK(cudaEventSynchronize(e1));
   float ms = 0.f;

@@ -109,6 +109,7 @@ template <int DIM, int EPI>
 __global__ void __launch_bounds__(BS) k_op(Grid g, Op<DIM> op, const double* __restrict__ x,
                                            const double* __restrict__ b, double* __restrict__ y,
                                            double* __restrict__ acc, double omega) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(BS) k_op(Grid g, Op<DIM> op, const double* __r
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_jacobi0(Grid g, Op<DIM> op, const double* __restrict__ b,
                                                 double* __restrict__ x, double omega) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(BS) k_jacobi0(Grid g, Op<DIM> op, const double
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_pre2(Grid g, Op<DIM> op, const double* __restrict__ r,
                                              double* __restrict__ e, double omega) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -195,6 +198,7 @@ __global__ void __launch_bounds__(BS) k_pre2(Grid g, Op<DIM> op, const double* _
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
                                                  double* __restrict__ rc) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= gc.N) return;
   const Node<DIM> nc = locate<DIM>(gc, idx);
@@ -219,6 +223,7 @@ __global__ void __launch_bounds__(BS) k_restrict(Grid gf, Grid gc, const double*
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec,
                                                     double* __restrict__ x) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= gf.N) return;
   const Node<DIM> nd = locate<DIM>(gf, idx);
@@ -238,6 +243,7 @@ __global__ void __launch_bounds__(BS) k_prolong_add(Grid gf, Grid gc, const doub
 __global__ void __launch_bounds__(BS) k_coarse_solve(int nc, const double* __restrict__ Ainv,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ y) {
+  PDL_ENTRY();
   const int row = blockIdx.x * (BS / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= nc) return;
@@ -260,6 +266,7 @@ __global__ void __launch_bounds__(BS) k_coarse_solve(int nc, const double* __res
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_cheb_first(Grid g, Op<DIM> A, const double* __restrict__ r,
                                                    double* __restrict__ d, double inv_theta) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -271,6 +278,7 @@ __global__ void __launch_bounds__(BS) k_cheb_step(Grid g, Op<DIM> A, const doubl
                                                   const double* r_in, const double* x_in,
                                                   double* __restrict__ d_out, double* r_out, double* x_out,
                                                   double c1, double c2, int last) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -382,6 +390,7 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_linearize(Grid g, Op<DIM> Kop, Nonlin nl, double eps2,
                                                   const double* __restrict__ u, double* __restrict__ coef,
                                                   size_t ldc) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -439,6 +448,7 @@ struct CArgs {
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(BS) k_capply(Grid g, Op<DIM> Mop, Op<DIM> Kop, Op<DIM> Aop, CArgs a,
                                                Reduce red) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   double nrm[1] = {0.0};
   if (idx < g.N) {
@@ -495,6 +505,7 @@ struct ResArgs {
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_residual(Grid g, Op<DIM> Mop, Op<DIM> Kop, Nonlin nl, ResArgs a,
                                                  Reduce red) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   double v[2] = {0.0, 0.0};
   if (idx < g.N) {
@@ -532,6 +543,7 @@ __global__ void __launch_bounds__(BS) k_residual(Grid g, Op<DIM> Mop, Op<DIM> Ko
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_nonlinear(Grid g, Nonlin nl, const double* __restrict__ u,
                                                   double* __restrict__ y) {
+  PDL_ENTRY();
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   if (idx >= g.N) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
@@ -548,6 +560,7 @@ template <int NVB>
 __global__ void __launch_bounds__(BS) k_arnoldi_dot(int nv, const double* __restrict__ w,
                                                     const double* __restrict__ V, size_t ldv, size_t n,
                                                     Reduce red) {
+  PDL_ENTRY();
   double acc[NVB + 1];
 #pragma unroll
   for (int q = 0; q <= NVB; ++q) acc[q] = 0.0;
@@ -567,6 +580,7 @@ __global__ void __launch_bounds__(BS) k_arnoldi_update(int nv, const double* __r
                                                        const double* __restrict__ V, size_t ldv, size_t n,
                                                        const double* __restrict__ h, double* __restrict__ w_out,
                                                        Reduce red) {
+  PDL_ENTRY();
   constexpr int NR = MODE == 0 ? NVB : 1;
   double hq[NVB];
 #pragma unroll
@@ -598,6 +612,7 @@ __global__ void __launch_bounds__(BS) k_arnoldi_update(int nv, const double* __r
 // y = x * (1/sqrt(*nrm2))  written to y1 (and y2 if non-null)
 __global__ void __launch_bounds__(BS) k_normalize(const double* __restrict__ x, const double* __restrict__ nrm2,
                                                   double* __restrict__ y1, double* __restrict__ y2, size_t n) {
+  PDL_ENTRY();
   const double s = 1.0 / sqrt(*nrm2);
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) {
     const double v = __ldg(x + i) * s;
@@ -612,6 +627,7 @@ struct Coeffs32 {
 // u = sum_q y_q V_q  (axpy sequence from zero, krylov.hpp:131-132)
 __global__ void __launch_bounds__(BS) k_combine(int nv, Coeffs32 y, const double* __restrict__ V, size_t ldv,
                                                 size_t n, double* __restrict__ u) {
+  PDL_ENTRY();
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) {
     double s = 0.0;
     for (int q = 0; q < nv; ++q) s = s + y.c[q] * __ldg(V + q * ldv + i);
@@ -622,6 +638,7 @@ __global__ void __launch_bounds__(BS) k_combine(int nv, Coeffs32 y, const double
 // y = a*x + y
 __global__ void __launch_bounds__(BS) k_axpy(double a, const double* __restrict__ x, double* __restrict__ y,
                                              size_t n) {
+  PDL_ENTRY();
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS)
     y[i] = y[i] + a * x[i];
 }
@@ -629,12 +646,14 @@ __global__ void __launch_bounds__(BS) k_axpy(double a, const double* __restrict_
 // y = x * s
 __global__ void __launch_bounds__(BS) k_scale(double s, const double* __restrict__ x, double* __restrict__ y,
                                               size_t n) {
+  PDL_ENTRY();
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) y[i] = x[i] * s;
 }
 
 // dot products of pairs (single value)
 __global__ void __launch_bounds__(BS) k_dot(const double* __restrict__ a, const double* __restrict__ b, size_t n,
                                             Reduce red) {
+  PDL_ENTRY();
   double acc[1] = {0.0};
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS)
     acc[0] = fma(__ldg(a + i), __ldg(b + i), acc[0]);
@@ -643,6 +662,7 @@ __global__ void __launch_bounds__(BS) k_dot(const double* __restrict__ a, const 
 
 // any non-finite entry -> *flag = 1
 __global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ x, size_t n, int* flag) {
+  PDL_ENTRY();
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS)
     if (!isfinite(x[i])) *flag = 1;
 }

@@ -59,6 +59,7 @@ __device__ __forceinline__ double tail_row(const TailLevel<DIM>& L, uint32_t idx
 
 template <int DIM>
 __global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> Ap) {
+  PDL_ENTRY();
   constexpr int NO = Traits<DIM>::NOFF;
   const int tid = threadIdx.x;
   __shared__ TailArgs<DIM> A;

@@ -138,6 +138,7 @@ __device__ __forceinline__ void epilogue_pre(const TArgs& a, uint32_t idx, doubl
 // thread computes TI vertices along x.  Extra CTAs take the boundary list.
 template <int DIM, int LOAD, int EPI, int TI>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
+  PDL_ENTRY();
   using TC = TileCfg<DIM>;
   constexpr int NO = Traits<DIM>::NOFF;
   const int tid = threadIdx.x;
