@@ -34,7 +34,7 @@ OPS = [("M", _lib.OP_M), ("K", _lib.OP_K), ("A", _lib.OP_A), ("VCYCLE", _lib.OP_
 # kernel-path modes: default choice; shared-memory tiled kernels forced on every
 # level (no single-CTA tail); one-thread-per-vertex kernels + the largest tail
 MODES = {"default": {}, "tiled": dict(tiled_min_n=2, tail_max_vertices=-1),
-         "tail": dict(tiled_min_n=-1, tail_max_vertices=1 << 30)}
+         "tail": dict(tiled_min_n=-1, tail_max_vertices=1 << 30, pdl=False)}
 
 
 @pytest.fixture(scope="module", params=[(c, m) for c in golden_cases() for m in MODES],
