@@ -143,27 +143,37 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled_c(Grid g, Op<DIM> Mo
       pb2[t] = (MODE == TC_JAC_RES && ok) ? a.b[a.n2 + idx] : 0.0;
     }
     const int per = (TI + 2) * TC::PSZ;
+    const int tot1 = (ni + 2) * TC::PSZ;
+    const int total = NOPS * per;
+    constexpr int U = 8;
+    for (int base = tid; base < total; base += TC::NT * U) {
+      double vv[U];
 #pragma unroll
-    for (int rr = 0; rr < (TC::PSZ + TC::NT - 1) / TC::NT; ++rr) {
-      const int r = tid + rr * TC::NT;
-      if (r < TC::PSZ) {
-        const int hj = DIM == 3 ? r / TC::PW : 0;
-        const int hk = DIM == 3 ? r - hj * TC::PW : r;
-        const int gj = DIM == 3 ? j0 - 1 + hj : 0;
-        const int gk = k0 - 1 + hk;
-        const bool ok = gk <= g.n && gj <= g.n;
-        const uint32_t lin0 = DIM == 3 ? (uint32_t)(i0 - 1) * g.ps + (uint32_t)gj * g.s + gk
-                                       : (uint32_t)(i0 - 1) * g.s + gk;
-#pragma unroll
-        for (int op = 0; op < NOPS; ++op) {
-          const double* src = op ? a.v : a.x;
-          double vv[TI + 2];
-#pragma unroll
-          for (int p = 0; p < TI + 2; ++p)
-            vv[p] = (ok && p < ni + 2) ? __ldg(src + lin0 + (uint32_t)p * pstride) : 0.0;
-#pragma unroll
-          for (int p = 0; p < TI + 2; ++p) tile[op * per + p * TC::PSZ + r] = vv[p];
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * TC::NT;
+        vv[u] = 0.0;
+        if (e < total) {
+          const int op = e >= per ? 1 : 0;
+          const int e2 = e - op * per;
+          if (e2 < tot1) {
+            const int p = e2 / TC::PSZ;
+            const int r = e2 - p * TC::PSZ;
+            const int hj = DIM == 3 ? r / TC::PW : 0;
+            const int hk = DIM == 3 ? r - hj * TC::PW : r;
+            const int gj = DIM == 3 ? j0 - 1 + hj : 0;
+            const int gk = k0 - 1 + hk;
+            const int ip = i0 - 1 + p;
+            if (gk <= g.n && gj <= g.n) {
+              const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
+              vv[u] = __ldg((op ? a.v : a.x) + lin);
+            }
+          }
         }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * TC::NT;
+        if (e < total) tile[e] = vv[u];
       }
     }
     __syncthreads();
