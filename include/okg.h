@@ -63,8 +63,11 @@ typedef struct okg_params {
                                kernels; 0 = default (3D: 32, 2D: 128), < 0 = never */
   int32_t tail_max_vertices;/* multigrid levels (below the finest) with at most this many
                                vertices run as ONE single-CTA V-cycle kernel;
-                               0 = default (1100), < 0 = never */
+                               0 = default (never), > 0 = threshold */
   int32_t disable_pdl;      /* 1: launch without programmatic dependent launch */
+  int32_t mg_fuse;          /* temporally blocked V(2,2) level kernels (one "down" and one
+                               "up" launch per level): 0 = default (all but the finest
+                               level), 1 = every level, < 0 = never */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */

@@ -70,7 +70,8 @@ class SolverConfig:
         return s ** self.dim
 
     def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
-                  tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True) -> _lib.Params:
+                  tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
+                  mg_fuse: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -83,6 +84,7 @@ class SolverConfig:
         p.tiled_min_n = tiled_min_n
         p.tail_max_vertices = tail_max_vertices
         p.disable_pdl = 0 if pdl else 1
+        p.mg_fuse = mg_fuse
         return p
 
     def validate(self) -> None:
@@ -231,13 +233,14 @@ class DeviceArray:
 class SchurContext:
     def __init__(self, cfg: SolverConfig, device: int = 0, shat_perturb: float = 0.0,
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
-                 pdl: bool = True):
+                 pdl: bool = True, mg_fuse: int = 0):
         if cfg.cheby_precond != "jacobi":
             raise ConfigError("schur context: only cheby_precond = 'jacobi' is implemented on the GPU path")
         self.cfg = cfg
         self.device = device
         self.handle = C.c_void_p()
-        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl)),
+        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl,
+                                                    mg_fuse)),
                              C.byref(self.handle)))
         info = _lib.Info()
         check(lib.okg_get_info(self.handle, C.byref(info)))

@@ -44,6 +44,7 @@ class Params(C.Structure):
         ("shat_perturb", C.c_double), ("max_dofs", C.c_int64),
         ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
         ("tail_max_vertices", C.c_int32), ("disable_pdl", C.c_int32),
+        ("mg_fuse", C.c_int32),
     ]
 
 

@@ -79,6 +79,7 @@ struct Level {
   Grid g;
   HostOp shat;
   bool tiled = false;
+  bool fused = false;  // V(2,2) through k_mg_down / k_mg_up (okg_vcycle.cuh)
   Tiling tl{};
   unsigned tl_blocks = 0;
   double *b = nullptr, *x = nullptr, *ea = nullptr, *eb = nullptr, *res = nullptr;
@@ -399,6 +400,19 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   }
   const double om = c->p.mg_omega;
   const Op<DIM> op = dev_op<DIM>(L.shat);
+  if (L.fused) {  // V(2,2) in two launches (okg_vcycle.cuh)
+    Level& C = c->lv[l + 1];
+    launch(c, k_mg_down<DIM>, mg_boxes<DIM>(L.g), MgBox<DIM>::NT, mg_down_smem<DIM>(), L.g, C.g, op, om, rhs, L.ea,
+           C.b);
+    note(c);
+    mg_level<DIM>(c, l + 1, C.b, C.x, false);
+    if (acc) launch(c, k_mg_up<DIM, true>, mg_boxes<DIM>(L.g), MgBox<DIM>::NT, mg_up_smem<DIM>(), L.g, C.g, op, om,
+                    rhs, (const double*)L.ea, (const double*)C.x, out);
+    else launch(c, k_mg_up<DIM, false>, mg_boxes<DIM>(L.g), MgBox<DIM>::NT, mg_up_smem<DIM>(), L.g, C.g, op, om,
+                rhs, (const double*)L.ea, (const double*)C.x, out);
+    note(c);
+    return;
+  }
   double* cur = L.ea;
   double* oth = L.eb;
   const int pre = c->p.mg_pre, post = c->p.mg_post;
@@ -1013,7 +1027,7 @@ static void build(okg_ctx* c) {
       L.res = dalloc(c, nl);
     }
     // single-CTA tail for the small levels (okg_tail.cuh)
-    const int64_t tmax = p.tail_max_vertices == 0 ? 1100 : p.tail_max_vertices;
+    const int64_t tmax = p.tail_max_vertices;
     if (tmax > 0) {
       for (size_t l = 1; l < c->lv.size(); ++l)
         if ((int64_t)c->lv[l].g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL) {
@@ -1021,6 +1035,9 @@ static void build(okg_ctx* c) {
           break;
         }
     }
+    // temporally blocked down/up kernels for V(2,2) (okg_vcycle.cuh)
+    if (p.mg_pre == 2 && p.mg_post == 2 && p.mg_fuse >= 0)
+      for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l) c->lv[l].fused = true;
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
     const int tmin = p.tiled_min_n == 0 ? (DIM == 3 ? 32 : 128) : p.tiled_min_n;
     if (tmin > 0)

@@ -670,3 +670,4 @@ __global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ 
 }  // namespace okg
 
 #include "okg_tiled_c.cuh"
+#include "okg_vcycle.cuh"

@@ -33,8 +33,8 @@ OPS = [("M", _lib.OP_M), ("K", _lib.OP_K), ("A", _lib.OP_A), ("VCYCLE", _lib.OP_
 
 # kernel-path modes: default choice; shared-memory tiled kernels forced on every
 # level (no single-CTA tail); one-thread-per-vertex kernels + the largest tail
-MODES = {"default": {}, "tiled": dict(tiled_min_n=2, tail_max_vertices=-1),
-         "tail": dict(tiled_min_n=-1, tail_max_vertices=1 << 30, pdl=False)}
+MODES = {"default": {}, "tiled": dict(tiled_min_n=2, tail_max_vertices=-1, mg_fuse=1),
+         "tail": dict(tiled_min_n=-1, tail_max_vertices=1 << 30, pdl=False, mg_fuse=-1)}
 
 
 @pytest.fixture(scope="module", params=[(c, m) for c in golden_cases() for m in MODES],
@@ -340,3 +340,18 @@ def test_solver_knobs_match_oracle(port_lib, kw, dim, n, mode):
     assert abs(r.iterations - ro["iterations"]) <= 1 and r.converged == ro["converged"]
     assert relerr(r.x, ro["x"]) <= FIELD_TOL
     ctx.close()
+
+
+@pytest.mark.parametrize("dim,n", [(2, 64), (3, 32), (3, 16)])
+def test_fused_vcycle_bit_identical(dim, n):
+    # okg_vcycle.cuh claims the same arithmetic per vertex as the unfused kernels
+    cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, min_coarse_size=10)
+    rng = np.random.default_rng(5)
+    outs = []
+    for mode in (dict(mg_fuse=-1), dict(mg_fuse=1), dict(mg_fuse=0)):
+        ctx = okg.SchurContext(cfg, **mode)
+        x = rng.uniform(-1, 1, ctx.n) if not outs else outs[0][0]
+        outs.append((x, ctx.apply(_lib.OP_VCYCLE, x), ctx.apply(_lib.OP_SHAT_INV, x)))
+        ctx.close()
+    for o in outs[1:]:
+        assert np.array_equal(o[1], outs[0][1]) and np.array_equal(o[2], outs[0][2])

@@ -16,7 +16,8 @@ seed = int(sys.argv[4]) if len(sys.argv) > 4 else (2 if dim == 3 else 0)
 cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30)
 ctx = okg.SchurContext(cfg, tiled_min_n=int(os.environ.get("OKG_TILED", "0")),
                        tail_max_vertices=int(os.environ.get("OKG_TAIL", "0")),
-                       pdl=os.environ.get("OKG_PDL", "1") == "1")
+                       pdl=os.environ.get("OKG_PDL", "1") == "1",
+                       mg_fuse=int(os.environ.get("OKG_FUSE", "0")))
 print(f"levels={ctx.level_sizes} tiled={ctx.tiled_levels} tail_start={ctx.tail_start}", flush=True)
 ctx.set_state(okg.State(okg.seeded_ic(ctx.n, seed, 0.0), np.zeros(ctx.n)))
 setup = _lib.lib.okg_kernel_launch_count()
