@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(BS) k_op(Grid g, Op<DIM> op, const double* __r
   } else if (EPI == EPI_RESID) {
     y[idx] = b[idx] - ax;
   } else {
-    const double e = x[idx] + omega * op_invd<DIM>(op, nd.cls) * (b[idx] - ax);
+    const double e = fma(omega * op_invd<DIM>(op, nd.cls), b[idx] - ax, x[idx]);
     if (EPI == EPI_JACOBI) y[idx] = e;
     else if (EPI == EPI_JACOBI_SET) acc[idx] = e;
     else acc[idx] = acc[idx] + e;
@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(BS) k_pre2(Grid g, Op<DIM> op, const double* _
   }
   const double wd = omega * op_invd<DIM>(op, nd.cls);
   const double ri = r[idx];
-  const double e1 = wd * ri;
-  e[idx] = e1 + wd * (ri - s);
+  const double e1 = __dmul_rn(wd, ri);
+  e[idx] = fma(wd, ri - s, e1);
 }
 
 // Restriction rc = P^T rf (spmv_transpose, sparse.hpp:159-169): the coarse
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(BS) k_cheb_step(Grid g, Op<DIM> A, const doubl
   const double ad = op_row<DIM>(A, g, idx, nd.cls, [&](uint32_t j) { return __ldg(d + j); });
   const double r = r_in[idx] - ad;
   const double z = r * op_invd<DIM>(A, nd.cls);
-  const double dn = c1 * d[idx] + c2 * z;
+  const double dn = fma(c1, d[idx], c2 * z);
   x_out[idx] = x_in[idx] + dn;
   if (!last) {
     d_out[idx] = dn;

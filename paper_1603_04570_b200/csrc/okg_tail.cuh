@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> 
           const Node<DIM> nd = locate<DIM>(L.g, i);
           double own = 0.0;
           const double As = tail_row<DIM>(L, i, nd, own, [&](uint32_t v, int, int, int) { return c[v]; });
-          o[i] = own + om * L.op.tab[nd.cls * (NO + 1) + NO] * (rhs[i] - As);
+          o[i] = fma(om * L.op.tab[nd.cls * (NO + 1) + NO], rhs[i] - As, own);
         }
         double* t = c;
         c = o;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> 
         const Node<DIM> nd = locate<DIM>(L.g, i);
         double own = 0.0;
         const double As = tail_row<DIM>(L, i, nd, own, [&](uint32_t v, int, int, int) { return c[v]; });
-        to[i] = own + om * L.op.tab[nd.cls * (NO + 1) + NO] * (rhs[i] - As);
+        to[i] = fma(om * L.op.tab[nd.cls * (NO + 1) + NO], rhs[i] - As, own);
       }
       double* t = c;
       c = o;

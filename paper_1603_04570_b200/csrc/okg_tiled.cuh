@@ -119,14 +119,14 @@ __device__ __forceinline__ void epilogue_pre(const TArgs& a, uint32_t idx, doubl
   } else if (EPI == T_CHEB) {
     const double r = bv - As;
     const double z = r * invd;
-    const double dn = a.c1 * s_own + a.c2 * z;
+    const double dn = fma(a.c1, s_own, a.c2 * z);
     a.acc[idx] = pv + dn;
     if (!a.last) {
       a.y2[idx] = dn;
       a.y[idx] = r;
     }
   } else {
-    const double e = s_own + a.omega * invd * (bv - As);
+    const double e = fma(a.omega * invd, bv - As, s_own);
     if (EPI == T_JACOBI) a.y[idx] = e;
     else if (EPI == T_JACOBI_SET) a.acc[idx] = e;
     else a.acc[idx] = pv + e;

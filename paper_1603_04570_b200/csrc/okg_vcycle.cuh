@@ -30,50 +30,37 @@ struct MgBox<2> {
   static constexpr int FI = 8, FJ = 1, FK = 64, NT = 256;
 };
 
-// a box region [o_i, o_i+ni) x [o_j, o_j+nj) x [o_k, o_k+nk) of the level grid
+// a box region [o_i, o_i+NI) x [o_j, o_j+NJ) x [o_k, o_k+NK) of the level grid,
+// extents known at compile time: the box F grown by HALO (minus LO on the high side)
+template <int DIM, int HALO, int LO>
 struct Reg {
-  int oi, oj, ok;
-  int ni, nj, nk;
-};
-
-template <int DIM>
-__device__ __forceinline__ Reg make_reg(int fi0, int fj0, int fk0, int halo, int lo_extra) {
-  // region covering [f0 - halo, f0 + F - 1 + halo - lo_extra]... (see callers)
   using B = MgBox<DIM>;
-  Reg r;
-  r.oi = fi0 - halo;
-  r.oj = DIM == 3 ? fj0 - halo : 0;
-  r.ok = fk0 - halo;
-  r.ni = B::FI + 2 * halo - lo_extra;
-  r.nj = DIM == 3 ? B::FJ + 2 * halo - lo_extra : 1;
-  r.nk = B::FK + 2 * halo - lo_extra;
-  return r;
-}
-
-template <int DIM>
-__device__ __forceinline__ int reg_size(const Reg& r) {
-  return r.ni * r.nj * r.nk;
-}
-
-// local index e -> global coords (i, j, k); k is the fastest coordinate in 2D too
-template <int DIM>
-__device__ __forceinline__ void reg_coords(const Reg& r, int e, int& i, int& j, int& k) {
-  const int a = e / r.nk;
-  k = r.ok + (e - a * r.nk);
-  if (DIM == 3) {
-    const int b = a / r.nj;
-    j = r.oj + (a - b * r.nj);
-    i = r.oi + b;
-  } else {
-    j = 0;
-    i = r.oi + a;
+  static constexpr int NI = B::FI + 2 * HALO - LO;
+  static constexpr int NJ = DIM == 3 ? B::FJ + 2 * HALO - LO : 1;
+  static constexpr int NK = B::FK + 2 * HALO - LO;
+  static constexpr int SIZE = NI * NJ * NK;
+  int oi, oj, ok;
+  __device__ Reg(int fi0, int fj0, int fk0) : oi(fi0 - HALO), oj(DIM == 3 ? fj0 - HALO : 0), ok(fk0 - HALO) {}
+  // local index e -> global coords (k is the fastest coordinate, also in 2D)
+  __device__ __forceinline__ void coords(int e, int& i, int& j, int& k) const {
+    const int a = e / NK;
+    k = ok + (e - a * NK);
+    if (DIM == 3) {
+      const int b = a / NJ;
+      j = oj + (a - b * NJ);
+      i = oi + b;
+    } else {
+      j = 0;
+      i = oi + a;
+    }
   }
-}
-
-template <int DIM>
-__device__ __forceinline__ int reg_index(const Reg& r, int i, int j, int k) {
-  return DIM == 3 ? ((i - r.oi) * r.nj + (j - r.oj)) * r.nk + (k - r.ok) : (i - r.oi) * r.nk + (k - r.ok);
-}
+  __device__ __forceinline__ int index(int i, int j, int k) const {
+    return DIM == 3 ? ((i - oi) * NJ + (j - oj)) * NK + (k - ok) : (i - oi) * NK + (k - ok);
+  }
+  __device__ __forceinline__ bool contains(int i, int j, int k) const {
+    return i >= oi && i < oi + NI && k >= ok && k < ok + NK && (DIM == 2 || (j >= oj && j < oj + NJ));
+  }
+};
 
 template <int DIM>
 __device__ __forceinline__ bool in_grid(const Grid& g, int i, int j, int k) {
@@ -86,12 +73,12 @@ __device__ __forceinline__ uint32_t lin_of(const Grid& g, int i, int j, int k) {
 }
 
 // A s at vertex (i,j,k) of class cls, s read from region buffer `src` (region rs)
-template <int DIM>
-__device__ __forceinline__ double reg_row(const Op<DIM>& op, int cls, const double* src, const Reg& rs, int i, int j,
+template <int DIM, class RS>
+__device__ __forceinline__ double reg_row(const Op<DIM>& op, int cls, const double* src, const RS& rs, int i, int j,
                                           int k, double& own) {
   constexpr int NO = Traits<DIM>::NOFF;
-  const int c = reg_index<DIM>(rs, i, j, k);
-  const int sj = DIM == 3 ? rs.nk : 0, si = DIM == 3 ? rs.nj * rs.nk : rs.nk;
+  const int c = rs.index(i, j, k);
+  constexpr int sj = DIM == 3 ? RS::NK : 0, si = DIM == 3 ? RS::NJ * RS::NK : RS::NK;
   double As = 0.0;
   if (cls == Traits<DIM>::INTERIOR) {
 #pragma unroll
@@ -140,6 +127,8 @@ __device__ __forceinline__ void box_origin(const Grid& g, int& fi0, int& fj0, in
 // and bc = P^T (b - A e2) (level l+1).
 //   S = F+3 : e1 = w D^-1 b          E = F+2 : e2 (and b)
 //   R = F+1 (low side) : r           coarse points 2G in F : bc
+// Staging loads are batched (U in flight per thread); the later phases read
+// shared memory only.
 // ---------------------------------------------------------------------------
 template <int DIM>
 __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_down(Grid g, Grid gc, Op<DIM> op, double omega,
@@ -147,46 +136,53 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_down(Grid g, Grid gc, Op<
                                                             double* __restrict__ bc) {
   PDL_ENTRY();
   using B = MgBox<DIM>;
+  using RS = Reg<DIM, 3, 0>;
+  using RE = Reg<DIM, 2, 0>;
+  using RR = Reg<DIM, 1, 1>;
   extern __shared__ double sm[];
   int fi0, fj0, fk0;
   box_origin<DIM>(g, fi0, fj0, fk0);
-  const Reg S = make_reg<DIM>(fi0, fj0, fk0, 3, 0);
-  const Reg E = make_reg<DIM>(fi0, fj0, fk0, 2, 0);
-  Reg R = make_reg<DIM>(fi0, fj0, fk0, 1, 1);  // [f0-1, f0+F-1]
-  double* se1 = sm;                          // |S|
-  double* sb = se1 + reg_size<DIM>(S);       // |E|
-  double* se2 = sb + reg_size<DIM>(E);       // |E|
-  double* sr = se1;                          // |R| overlays e1 after phase 2
+  const RS S(fi0, fj0, fk0);
+  const RE E(fi0, fj0, fk0);
+  const RR R(fi0, fj0, fk0);
+  double* se1 = sm;            // |S|
+  double* sb = se1 + RS::SIZE; // |E|
+  double* se2 = sb + RE::SIZE; // |E|
+  double* sr = se1;            // |R| overlays e1 after phase 2
   const int tid = threadIdx.x;
-  // phase 1: e1 on S, b on E
-  for (int e = tid; e < reg_size<DIM>(S); e += B::NT) {
-    int i, j, k;
-    reg_coords<DIM>(S, e, i, j, k);
-    double v = 0.0;
-    if (in_grid<DIM>(g, i, j, k)) {
-      const double bv = __ldg(b + lin_of<DIM>(g, i, j, k));
-      v = omega * cls_invd<DIM>(op, class_of<DIM>(g, i, j, k)) * bv;
-      const bool inE = i >= E.oi && i < E.oi + E.ni && k >= E.ok && k < E.ok + E.nk &&
-                       (DIM == 2 || (j >= E.oj && j < E.oj + E.nj));
-      if (inE) sb[reg_index<DIM>(E, i, j, k)] = bv;
-    } else {
-      const bool inE = i >= E.oi && i < E.oi + E.ni && k >= E.ok && k < E.ok + E.nk &&
-                       (DIM == 2 || (j >= E.oj && j < E.oj + E.nj));
-      if (inE) sb[reg_index<DIM>(E, i, j, k)] = 0.0;
+  constexpr int U = 8;
+  // phase 1: e1 on S, b on E (batched loads)
+  for (int base = tid; base < RS::SIZE; base += B::NT * U) {
+    double bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * B::NT;
+      int i, j, k;
+      S.coords(e, i, j, k);
+      bv[u] = (e < RS::SIZE && in_grid<DIM>(g, i, j, k)) ? __ldg(b + lin_of<DIM>(g, i, j, k)) : 0.0;
     }
-    se1[e] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * B::NT;
+      if (e >= RS::SIZE) break;
+      int i, j, k;
+      S.coords(e, i, j, k);
+      const bool in = in_grid<DIM>(g, i, j, k);
+      se1[e] = in ? omega * cls_invd<DIM>(op, class_of<DIM>(g, i, j, k)) * bv[u] : 0.0;
+      if (E.contains(i, j, k)) sb[E.index(i, j, k)] = bv[u];
+    }
   }
   __syncthreads();
   // phase 2: e2 on E ; write e2 for the box F
-  for (int e = tid; e < reg_size<DIM>(E); e += B::NT) {
+  for (int e = tid; e < RE::SIZE; e += B::NT) {
     int i, j, k;
-    reg_coords<DIM>(E, e, i, j, k);
+    E.coords(e, i, j, k);
     double v = 0.0;
     if (in_grid<DIM>(g, i, j, k)) {
       const int cls = class_of<DIM>(g, i, j, k);
       double own = 0.0;
       const double As = reg_row<DIM>(op, cls, se1, S, i, j, k, own);
-      v = own + omega * cls_invd<DIM>(op, cls) * (sb[e] - As);
+      v = fma(omega * cls_invd<DIM>(op, cls), sb[e] - As, own);
       const bool inF = i >= fi0 && i < fi0 + B::FI && k >= fk0 && k < fk0 + B::FK &&
                        (DIM == 2 || (j >= fj0 && j < fj0 + B::FJ));
       if (inF) e2[lin_of<DIM>(g, i, j, k)] = v;
@@ -195,15 +191,15 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_down(Grid g, Grid gc, Op<
   }
   __syncthreads();
   // phase 3: residual on R
-  for (int e = tid; e < reg_size<DIM>(R); e += B::NT) {
+  for (int e = tid; e < RR::SIZE; e += B::NT) {
     int i, j, k;
-    reg_coords<DIM>(R, e, i, j, k);
+    R.coords(e, i, j, k);
     double v = 0.0;
     if (in_grid<DIM>(g, i, j, k)) {
       const int cls = class_of<DIM>(g, i, j, k);
       double own = 0.0;
       const double As = reg_row<DIM>(op, cls, se2, E, i, j, k, own);
-      v = sb[reg_index<DIM>(E, i, j, k)] - As;
+      v = sb[E.index(i, j, k)] - As;
     }
     sr[e] = v;
   }
@@ -215,8 +211,8 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_down(Grid g, Grid gc, Op<
     const int cj = DIM == 3 ? t % CJ : 0, ci = DIM == 3 ? t / CJ : t;
     const int Gi = fi0 / 2 + ci, Gj = DIM == 3 ? fj0 / 2 + cj : 0, Gk = fk0 / 2 + ck;
     if (!in_grid<DIM>(gc, Gi, Gj, Gk)) continue;
-    const int c = reg_index<DIM>(R, 2 * Gi, 2 * Gj, 2 * Gk);
-    const int sj = DIM == 3 ? R.nk : 0, si = DIM == 3 ? R.nj * R.nk : R.nk;
+    const int c = R.index(2 * Gi, 2 * Gj, 2 * Gk);
+    constexpr int sj = DIM == 3 ? RR::NK : 0, si = DIM == 3 ? RR::NJ * RR::NK : RR::NK;
     double s = 0.0;
 #pragma unroll
     for (int o = 0; o < Traits<DIM>::NOFF; ++o) {
@@ -238,40 +234,60 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_up(Grid g, Grid gc, Op<DI
                                                           const double* __restrict__ ec, double* __restrict__ out) {
   PDL_ENTRY();
   using B = MgBox<DIM>;
+  using RP = Reg<DIM, 2, 0>;
+  using RQ = Reg<DIM, 1, 0>;
   extern __shared__ double sm[];
   int fi0, fj0, fk0;
   box_origin<DIM>(g, fi0, fj0, fk0);
-  const Reg P = make_reg<DIM>(fi0, fj0, fk0, 2, 0);
-  const Reg Q = make_reg<DIM>(fi0, fj0, fk0, 1, 0);
+  const RP P(fi0, fj0, fk0);
+  const RQ Q(fi0, fj0, fk0);
   double* sp = sm;
-  double* sq = sp + reg_size<DIM>(P);
-  double* sbq = sq + reg_size<DIM>(Q);
+  double* sq = sp + RP::SIZE;
+  double* sbq = sq + RQ::SIZE;
   const int tid = threadIdx.x;
-  for (int e = tid; e < reg_size<DIM>(P); e += B::NT) {
-    int i, j, k;
-    reg_coords<DIM>(P, e, i, j, k);
-    double v = 0.0;
-    if (in_grid<DIM>(g, i, j, k)) {
-      const double t = prolong_at<DIM>(gc, ec, i, j, k);
-      v = __ldg(e2 + lin_of<DIM>(g, i, j, k)) + t;
+  constexpr int U = 8;
+  for (int base = tid; base < RP::SIZE; base += B::NT * U) {
+    double ev[U], tv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * B::NT;
+      int i, j, k;
+      P.coords(e, i, j, k);
+      const bool in = e < RP::SIZE && in_grid<DIM>(g, i, j, k);
+      ev[u] = in ? __ldg(e2 + lin_of<DIM>(g, i, j, k)) : 0.0;
+      tv[u] = in ? prolong_at<DIM>(gc, ec, i, j, k) : 0.0;
     }
-    sp[e] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * B::NT;
+      if (e < RP::SIZE) sp[e] = ev[u] + tv[u];
+    }
   }
-  for (int e = tid; e < reg_size<DIM>(Q); e += B::NT) {
-    int i, j, k;
-    reg_coords<DIM>(Q, e, i, j, k);
-    sbq[e] = in_grid<DIM>(g, i, j, k) ? __ldg(b + lin_of<DIM>(g, i, j, k)) : 0.0;
+  for (int base = tid; base < RQ::SIZE; base += B::NT * U) {
+    double bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * B::NT;
+      int i, j, k;
+      Q.coords(e, i, j, k);
+      bv[u] = (e < RQ::SIZE && in_grid<DIM>(g, i, j, k)) ? __ldg(b + lin_of<DIM>(g, i, j, k)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = base + u * B::NT;
+      if (e < RQ::SIZE) sbq[e] = bv[u];
+    }
   }
   __syncthreads();
-  for (int e = tid; e < reg_size<DIM>(Q); e += B::NT) {
+  for (int e = tid; e < RQ::SIZE; e += B::NT) {
     int i, j, k;
-    reg_coords<DIM>(Q, e, i, j, k);
+    Q.coords(e, i, j, k);
     double v = 0.0;
     if (in_grid<DIM>(g, i, j, k)) {
       const int cls = class_of<DIM>(g, i, j, k);
       double own = 0.0;
       const double As = reg_row<DIM>(op, cls, sp, P, i, j, k, own);
-      v = own + omega * cls_invd<DIM>(op, cls) * (sbq[e] - As);
+      v = fma(omega * cls_invd<DIM>(op, cls), sbq[e] - As, own);
     }
     sq[e] = v;
   }
@@ -283,7 +299,7 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_up(Grid g, Grid gc, Op<DI
     const int cls = class_of<DIM>(g, i, j, k);
     double own = 0.0;
     const double As = reg_row<DIM>(op, cls, sq, Q, i, j, k, own);
-    const double x = own + omega * cls_invd<DIM>(op, cls) * (sbq[reg_index<DIM>(Q, i, j, k)] - As);
+    const double x = fma(omega * cls_invd<DIM>(op, cls), sbq[Q.index(i, j, k)] - As, own);
     const uint32_t idx = lin_of<DIM>(g, i, j, k);
     if (ACC) out[idx] = out[idx] + x;
     else out[idx] = x;
