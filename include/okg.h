@@ -66,8 +66,9 @@ typedef struct okg_params {
                                0 = default (never), > 0 = threshold */
   int32_t disable_pdl;      /* 1: launch without programmatic dependent launch */
   int32_t mg_fuse;          /* temporally blocked V(2,2) level kernels (one "down" and one
-                               "up" launch per level): 0 = default (all but the finest
-                               level), 1 = every level, < 0 = never */
+                               "up" launch per level): 0 = default (2D: every level
+                               but the finest; 3D: levels with n <= 32), 1 = every
+                               level, < 0 = never */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */

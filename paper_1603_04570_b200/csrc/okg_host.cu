@@ -1036,8 +1036,11 @@ static void build(okg_ctx* c) {
         }
     }
     // temporally blocked down/up kernels for V(2,2) (okg_vcycle.cuh)
+    // default: every coarse level in 2D; in 3D the levels with n <= 32 (the halo-3
+    // redundancy of a 3D box outweighs the saved launches on bigger levels)
     if (p.mg_pre == 2 && p.mg_post == 2 && p.mg_fuse >= 0)
-      for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l) c->lv[l].fused = true;
+      for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l)
+        if (p.mg_fuse == 1 || DIM == 2 || c->lv[l].g.n <= 32) c->lv[l].fused = true;
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
     const int tmin = p.tiled_min_n == 0 ? (DIM == 3 ? 32 : 128) : p.tiled_min_n;
     if (tmin > 0)
