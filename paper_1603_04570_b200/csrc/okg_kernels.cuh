@@ -503,26 +503,50 @@ struct ResArgs {
 };
 
 template <int DIM>
+__device__ __forceinline__ double ring_row(const Op<DIM>& op, int cls, const double (&x)[Traits<DIM>::NOFF]) {
+  constexpr int NO = Traits<DIM>::NOFF;
+  double s = 0.0;
+  if (cls == Traits<DIM>::INTERIOR) {
+#pragma unroll
+    for (int o = 0; o < NO; ++o) s = fma(op.w[o], x[o], s);
+  } else {
+    const double* t = op.tab + cls * (NO + 1);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      const double w = __ldg(t + o);
+      if (w != 0.0) s = fma(w, x[o], s);
+    }
+  }
+  return s;
+}
+
+// Each state ring (u+, w+, u, w) is loaded once; every M/K row and N(u+)
+// is evaluated from registers.
+template <int DIM>
 __global__ void __launch_bounds__(BS) k_residual(Grid g, Op<DIM> Mop, Op<DIM> Kop, Nonlin nl, ResArgs a,
                                                  Reduce red) {
   PDL_ENTRY();
+  constexpr int NO = Traits<DIM>::NOFF;
   const uint32_t idx = blockIdx.x * BS + threadIdx.x;
   double v[2] = {0.0, 0.0};
   if (idx < g.N) {
     const Node<DIM> nd = locate<DIM>(g, idx);
     const double bi = nd.cls == Traits<DIM>::INTERIOR ? a.b_int : __ldg(a.b_tab + nd.cls);
-    const double mdu = op_row<DIM>(Mop, g, idx, nd.cls,
-                                   [&](uint32_t j) { return __ldg(a.un + j) - __ldg(a.uo + j); });
-    const double kwn = op_row<DIM>(Kop, g, idx, nd.cls, [&](uint32_t j) { return __ldg(a.wn + j); });
-    const double mun = op_row<DIM>(Mop, g, idx, nd.cls, [&](uint32_t j) { return __ldg(a.un + j); });
-    const double kwo = op_row<DIM>(Kop, g, idx, nd.cls, [&](uint32_t j) { return __ldg(a.wo + j); });
-    const double muo = op_row<DIM>(Mop, g, idx, nd.cls, [&](uint32_t j) { return __ldg(a.uo + j); });
-    const double mwn = op_row<DIM>(Mop, g, idx, nd.cls, [&](uint32_t j) { return __ldg(a.wn + j); });
-    double ul[Traits<DIM>::NOFF];
-    load_ring<DIM>(g, idx, nd.cls, a.un, ul);
-    const double kun = op_row<DIM>(Kop, g, idx, nd.cls,
-                                   [&](uint32_t j) { return __ldg(a.un + j); });
-    const double nlu = nonlinear_row<DIM>(g, nd, ul, nl);
+    double un[NO], wn[NO], uo[NO], wo[NO], du[NO];
+    load_ring<DIM>(g, idx, nd.cls, a.un, un);
+    load_ring<DIM>(g, idx, nd.cls, a.wn, wn);
+    load_ring<DIM>(g, idx, nd.cls, a.uo, uo);
+    load_ring<DIM>(g, idx, nd.cls, a.wo, wo);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) du[o] = un[o] - uo[o];
+    const double mdu = ring_row<DIM>(Mop, nd.cls, du);
+    const double kwn = ring_row<DIM>(Kop, nd.cls, wn);
+    const double mun = ring_row<DIM>(Mop, nd.cls, un);
+    const double kwo = ring_row<DIM>(Kop, nd.cls, wo);
+    const double muo = ring_row<DIM>(Mop, nd.cls, uo);
+    const double mwn = ring_row<DIM>(Mop, nd.cls, wn);
+    const double kun = ring_row<DIM>(Kop, nd.cls, un);
+    const double nlu = nonlinear_row<DIM>(g, nd, un, nl);
     const double fn = kwn + a.sigma * (mun + (-a.m) * bi);
     const double fo = kwo + a.sigma * (muo + (-a.m) * bi);
     double r1 = mdu;
@@ -555,7 +579,10 @@ __global__ void __launch_bounds__(BS) k_nonlinear(Grid g, Nonlin nl, const doubl
 // ---------------------------------------------------------------------------
 // Krylov vector kernels (grid-stride, fixed grid => deterministic sums).
 // ---------------------------------------------------------------------------
-// out[q] = V_q . w (q < nv), out[nv] = w . w
+// out[q] = V_q . w (q < nv), out[NVB] = w . w
+// All basis loads of an element are issued before any FMA (the compiler
+// otherwise recycles one register and serialises them); two elements per
+// thread per iteration for more bytes in flight.
 template <int NVB>
 __global__ void __launch_bounds__(BS) k_arnoldi_dot(int nv, const double* __restrict__ w,
                                                     const double* __restrict__ V, size_t ldv, size_t n,
@@ -564,12 +591,20 @@ __global__ void __launch_bounds__(BS) k_arnoldi_dot(int nv, const double* __rest
   double acc[NVB + 1];
 #pragma unroll
   for (int q = 0; q <= NVB; ++q) acc[q] = 0.0;
-  for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) {
-    const double wi = __ldg(w + i);
+  const size_t stride = (size_t)gridDim.x * BS;
+  for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += 2 * stride) {
+    const size_t i2 = i + stride;
+    const bool two = i2 < n;
+    double v1[NVB], v2[NVB];
 #pragma unroll
-    for (int q = 0; q < NVB; ++q)
-      if (q < nv) acc[q] = fma(__ldg(V + q * ldv + i), wi, acc[q]);
-    acc[NVB] = fma(wi, wi, acc[NVB]);
+    for (int q = 0; q < NVB; ++q) {
+      v1[q] = q < nv ? __ldg(V + q * ldv + i) : 0.0;
+      v2[q] = (q < nv && two) ? __ldg(V + q * ldv + i2) : 0.0;
+    }
+    const double w1 = __ldg(w + i), w2 = two ? __ldg(w + i2) : 0.0;
+#pragma unroll
+    for (int q = 0; q < NVB; ++q) acc[q] = fma(v2[q], w2, fma(v1[q], w1, acc[q]));
+    acc[NVB] = fma(w2, w2, fma(w1, w1, acc[NVB]));
   }
   grid_reduce<NVB + 1>(acc, red);
 }
@@ -590,18 +625,16 @@ __global__ void __launch_bounds__(BS) k_arnoldi_update(int nv, const double* __r
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) {
     double vi[NVB];
+#pragma unroll
+    for (int q = 0; q < NVB; ++q) vi[q] = q < nv ? __ldg(V + q * ldv + i) : 0.0;
     double x = __ldg(w + i);
 #pragma unroll
     for (int q = 0; q < NVB; ++q)
-      if (q < nv) {
-        vi[q] = __ldg(V + q * ldv + i);
-        x = x - hq[q] * vi[q];
-      }
+      if (q < nv) x = x - hq[q] * vi[q];
     w_out[i] = x;
     if (MODE == 0) {
 #pragma unroll
-      for (int q = 0; q < NVB; ++q)
-        if (q < nv) acc[q] = fma(vi[q], x, acc[q]);
+      for (int q = 0; q < NVB; ++q) acc[q] = fma(vi[q], x, acc[q]);
     } else {
       acc[0] = fma(x, x, acc[0]);
     }
@@ -629,8 +662,13 @@ __global__ void __launch_bounds__(BS) k_combine(int nv, Coeffs32 y, const double
                                                 size_t n, double* __restrict__ u) {
   PDL_ENTRY();
   for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) {
+    double vi[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) vi[q] = q < nv ? __ldg(V + q * ldv + i) : 0.0;
     double s = 0.0;
-    for (int q = 0; q < nv; ++q) s = s + y.c[q] * __ldg(V + q * ldv + i);
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if (q < nv) s = s + y.c[q] * vi[q];
     u[i] = s;
   }
 }
