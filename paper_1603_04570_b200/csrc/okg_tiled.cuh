@@ -227,9 +227,10 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
   }
   __syncthreads();
   if (!active) return;
+  // all TI vertex chains are computed unconditionally (no branch between them, so
+  // their dependent FMA chains interleave); only the stores are predicated
 #pragma unroll
   for (int t = 0; t < TI; ++t) {
-    if (t >= ni) break;
     double As = 0.0, s_own = 0.0;
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
       if (o == Traits<DIM>::CENTER) s_own = sv;
       As = fma(op.w[o], sv, As);
     }
-    epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, pb[t], pp[t]);
+    if (t < ni) epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, pb[t], pp[t]);
   }
 }
 

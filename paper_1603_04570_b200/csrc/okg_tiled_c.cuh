@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled_c(Grid g, Op<DIM> Mo
     if (active) {
 #pragma unroll
       for (int t = 0; t < TI; ++t) {
-        if (t >= ni) break;
+        if (t >= ni) continue;
         double xs[NO], vs[NO];
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
