@@ -382,6 +382,33 @@ static void run_tail(okg_ctx* c, int l0, const double* rhs, double* out) {
 }
 
 template <int DIM>
+static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc);
+
+template <int DIM, int BX>
+static void mg_fused(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
+  Level& L = c->lv[l];
+  Level& C = c->lv[l + 1];
+  const Op<DIM> op = dev_op<DIM>(L.shat);
+  const double om = c->p.mg_omega;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_mg_down<DIM, BX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mg_down_smem<DIM, BX>()));
+    CK(cudaFuncSetAttribute(k_mg_up<DIM, BX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mg_up_smem<DIM, BX>()));
+    CK(cudaFuncSetAttribute(k_mg_up<DIM, BX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mg_up_smem<DIM, BX>()));
+    attr = true;
+  }
+  launch(c, k_mg_down<DIM, BX>, mg_boxes<DIM, BX>(L.g), MgBox<DIM, BX>::NT, mg_down_smem<DIM, BX>(), L.g, C.g, op, om, rhs,
+         L.ea, C.b);
+  note(c);
+  mg_level<DIM>(c, l + 1, C.b, C.x, false);
+  if (acc) launch(c, k_mg_up<DIM, BX, true>, mg_boxes<DIM, BX>(L.g), MgBox<DIM, BX>::NT, mg_up_smem<DIM, BX>(), L.g, C.g,
+                  op, om, rhs, (const double*)L.ea, (const double*)C.x, out);
+  else launch(c, k_mg_up<DIM, BX, false>, mg_boxes<DIM, BX>(L.g), MgBox<DIM, BX>::NT, mg_up_smem<DIM, BX>(), L.g, C.g,
+              op, om, rhs, (const double*)L.ea, (const double*)C.x, out);
+  note(c);
+}
+
+template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
   Level& L = c->lv[l];
   const int last = static_cast<int>(c->lv.size()) - 1;
@@ -401,16 +428,8 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   const double om = c->p.mg_omega;
   const Op<DIM> op = dev_op<DIM>(L.shat);
   if (L.fused) {  // V(2,2) in two launches (okg_vcycle.cuh)
-    Level& C = c->lv[l + 1];
-    launch(c, k_mg_down<DIM>, mg_boxes<DIM>(L.g), MgBox<DIM>::NT, mg_down_smem<DIM>(), L.g, C.g, op, om, rhs, L.ea,
-           C.b);
-    note(c);
-    mg_level<DIM>(c, l + 1, C.b, C.x, false);
-    if (acc) launch(c, k_mg_up<DIM, true>, mg_boxes<DIM>(L.g), MgBox<DIM>::NT, mg_up_smem<DIM>(), L.g, C.g, op, om,
-                    rhs, (const double*)L.ea, (const double*)C.x, out);
-    else launch(c, k_mg_up<DIM, false>, mg_boxes<DIM>(L.g), MgBox<DIM>::NT, mg_up_smem<DIM>(), L.g, C.g, op, om,
-                rhs, (const double*)L.ea, (const double*)C.x, out);
-    note(c);
+    // BX = 1 (larger box) measured no better on the big levels; kept for experiments
+    mg_fused<DIM, 0>(c, l, rhs, out, acc);
     return;
   }
   double* cur = L.ea;

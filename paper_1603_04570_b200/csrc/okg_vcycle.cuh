@@ -18,23 +18,32 @@
 
 namespace okg {
 
-// fine box per CTA (even extents, aligned to the coarse grid)
-template <int DIM>
+// fine box per CTA (even extents, aligned to the coarse grid); BX = 1 is the
+// larger box used on big levels (less halo redundancy, fewer CTAs)
+template <int DIM, int BX = 0>
 struct MgBox;
 template <>
-struct MgBox<3> {
+struct MgBox<3, 0> {
   static constexpr int FI = 4, FJ = 4, FK = 16, NT = 256;
 };
 template <>
-struct MgBox<2> {
+struct MgBox<3, 1> {
+  static constexpr int FI = 4, FJ = 8, FK = 32, NT = 256;
+};
+template <>
+struct MgBox<2, 0> {
   static constexpr int FI = 8, FJ = 1, FK = 64, NT = 256;
+};
+template <>
+struct MgBox<2, 1> {
+  static constexpr int FI = 8, FJ = 1, FK = 128, NT = 256;
 };
 
 // a box region [o_i, o_i+NI) x [o_j, o_j+NJ) x [o_k, o_k+NK) of the level grid,
 // extents known at compile time: the box F grown by HALO (minus LO on the high side)
-template <int DIM, int HALO, int LO>
+template <int DIM, int HALO, int LO, int BX = 0>
 struct Reg {
-  using B = MgBox<DIM>;
+  using B = MgBox<DIM, BX>;
   static constexpr int NI = B::FI + 2 * HALO - LO;
   static constexpr int NJ = DIM == 3 ? B::FJ + 2 * HALO - LO : 1;
   static constexpr int NK = B::FK + 2 * HALO - LO;
@@ -108,9 +117,9 @@ __device__ __forceinline__ double cls_invd(const Op<DIM>& op, int cls) {
 }
 
 // box origin of this CTA (fine coordinates)
-template <int DIM>
+template <int DIM, int BX>
 __device__ __forceinline__ void box_origin(const Grid& g, int& fi0, int& fj0, int& fk0) {
-  using B = MgBox<DIM>;
+  using B = MgBox<DIM, BX>;
   const int nbk = g.n / B::FK + 1, nbj = DIM == 3 ? g.n / B::FJ + 1 : 1;
   int b = blockIdx.x;
   const int bk = b % nbk;
@@ -130,18 +139,18 @@ __device__ __forceinline__ void box_origin(const Grid& g, int& fi0, int& fj0, in
 // Staging loads are batched (U in flight per thread); the later phases read
 // shared memory only.
 // ---------------------------------------------------------------------------
-template <int DIM>
-__global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_down(Grid g, Grid gc, Op<DIM> op, double omega,
-                                                            const double* __restrict__ b, double* __restrict__ e2,
-                                                            double* __restrict__ bc) {
+template <int DIM, int BX>
+__global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc, Op<DIM> op, double omega,
+                                                                const double* __restrict__ b, double* __restrict__ e2,
+                                                                double* __restrict__ bc) {
   PDL_ENTRY();
-  using B = MgBox<DIM>;
-  using RS = Reg<DIM, 3, 0>;
-  using RE = Reg<DIM, 2, 0>;
-  using RR = Reg<DIM, 1, 1>;
+  using B = MgBox<DIM, BX>;
+  using RS = Reg<DIM, 3, 0, BX>;
+  using RE = Reg<DIM, 2, 0, BX>;
+  using RR = Reg<DIM, 1, 1, BX>;
   extern __shared__ double sm[];
   int fi0, fj0, fk0;
-  box_origin<DIM>(g, fi0, fj0, fk0);
+  box_origin<DIM, BX>(g, fi0, fj0, fk0);
   const RS S(fi0, fj0, fk0);
   const RE E(fi0, fj0, fk0);
   const RR R(fi0, fj0, fk0);
@@ -228,17 +237,17 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_down(Grid g, Grid gc, Op<
 // UP: coarse correction + two post-sweeps.  out = x (SET) or out += x (ACC).
 //   P = F+2 : e = e2 + P e_c        Q = F+1 : e'        F : x
 // ---------------------------------------------------------------------------
-template <int DIM, bool ACC>
-__global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_up(Grid g, Grid gc, Op<DIM> op, double omega,
-                                                          const double* __restrict__ b, const double* __restrict__ e2,
-                                                          const double* __restrict__ ec, double* __restrict__ out) {
+template <int DIM, int BX, bool ACC>
+__global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, Op<DIM> op, double omega,
+                                                              const double* __restrict__ b, const double* __restrict__ e2,
+                                                              const double* __restrict__ ec, double* __restrict__ out) {
   PDL_ENTRY();
-  using B = MgBox<DIM>;
-  using RP = Reg<DIM, 2, 0>;
-  using RQ = Reg<DIM, 1, 0>;
+  using B = MgBox<DIM, BX>;
+  using RP = Reg<DIM, 2, 0, BX>;
+  using RQ = Reg<DIM, 1, 0, BX>;
   extern __shared__ double sm[];
   int fi0, fj0, fk0;
-  box_origin<DIM>(g, fi0, fj0, fk0);
+  box_origin<DIM, BX>(g, fi0, fj0, fk0);
   const RP P(fi0, fj0, fk0);
   const RQ Q(fi0, fj0, fk0);
   double* sp = sm;
@@ -306,21 +315,21 @@ __global__ void __launch_bounds__(MgBox<DIM>::NT) k_mg_up(Grid g, Grid gc, Op<DI
   }
 }
 
-template <int DIM>
+template <int DIM, int BX>
 inline unsigned mg_boxes(const Grid& g) {
-  using B = MgBox<DIM>;
+  using B = MgBox<DIM, BX>;
   return (unsigned)((g.n / B::FK + 1) * (DIM == 3 ? g.n / B::FJ + 1 : 1) * (g.n / B::FI + 1));
 }
-template <int DIM>
+template <int DIM, int BX>
 inline size_t mg_down_smem() {
-  using B = MgBox<DIM>;
+  using B = MgBox<DIM, BX>;
   const size_t s = (size_t)(B::FI + 6) * (DIM == 3 ? B::FJ + 6 : 1) * (B::FK + 6);
   const size_t e = (size_t)(B::FI + 4) * (DIM == 3 ? B::FJ + 4 : 1) * (B::FK + 4);
   return (s + 2 * e) * sizeof(double);
 }
-template <int DIM>
+template <int DIM, int BX>
 inline size_t mg_up_smem() {
-  using B = MgBox<DIM>;
+  using B = MgBox<DIM, BX>;
   const size_t p = (size_t)(B::FI + 4) * (DIM == 3 ? B::FJ + 4 : 1) * (B::FK + 4);
   const size_t q = (size_t)(B::FI + 2) * (DIM == 3 ? B::FJ + 2 : 1) * (B::FK + 2);
   return (p + 2 * q) * sizeof(double);
