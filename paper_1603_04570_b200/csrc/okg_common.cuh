@@ -106,8 +106,10 @@ struct Grid {
   int32_t n;    // cells per axis
   int32_t s;    // n + 1
   uint32_t ps;  // plane size s^(dim-1)
-  uint32_t N;   // vertices
-  int32_t off[15];  // linear offsets of the stencil slots
+  uint32_t N;   // vertices of the whole level
+  int32_t ilo, ihi;  // owned x-planes [ilo, ihi) of this slab (whole grid: 0, s)
+  uint32_t lo, hi;   // owned linear range [ilo*ps, ihi*ps)
+  int32_t off[15];   // linear offsets of the stencil slots
 };
 
 // Constant stencil by value: interior row in the parameter bank, boundary

@@ -22,8 +22,12 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/okg.h"
@@ -76,7 +80,10 @@ static Op<DIM> dev_op(const HostOp& h) {
 }
 
 struct Level {
-  Grid g;
+  Grid g;      // owned planes [g.ilo, g.ihi) of this slab (the whole level when not split)
+  int gh = 0;  // ghost planes per side (1 on split levels of a multi-slab context)
+  size_t B = 0;     // allocation stride of one level vector (owned + ghost planes)
+  bool rep = false; // replicated on every slab (levels too thin to split, the coarsest)
   HostOp shat;
   bool tiled = false;
   bool fused = false;  // V(2,2) through k_mg_down / k_mg_up (okg_vcycle.cuh)
@@ -84,6 +91,8 @@ struct Level {
   unsigned tl_blocks = 0;
   double *b = nullptr, *x = nullptr, *ea = nullptr, *eb = nullptr, *res = nullptr;
 };
+
+struct Group;
 
 }  // namespace okg
 
@@ -136,6 +145,16 @@ struct okg_ctx {
   int cap_count = 0;
   std::vector<void*> allocs;
   size_t bytes = 0;
+  // slab decomposition (see okg_group section below); one slab: rank 0 of 1
+  int rank = 0, nslabs = 1;
+  okg::Group* group = nullptr;
+  size_t B = 0;        // fine-level vector stride (== N without ghost planes)
+  ptrdiff_t foff = 0;  // flat pointer of a fine-level vector = global-indexed pointer + foff
+  Seg seg{};           // owned entries of a stacked fine vector
+  int L_rep = 1 << 30; // first replicated level
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::vector<std::pair<double*, int>> reg;  // exchange registry: (global-indexed pointer, level)
+  std::vector<okg_ctx*> slabs;               // set only on the handle of a multi-slab context
 };
 
 namespace okg {
@@ -152,6 +171,17 @@ static double* dalloc(okg_ctx* c, size_t n) {
   c->allocs.push_back(p);
   c->bytes += n * sizeof(double);
   return static_cast<double*>(p);
+}
+
+// A level vector: owned planes plus gh ghost planes per side, returned as a
+// GLOBAL-INDEXED pointer (p[global vertex index] is valid for planes
+// [ilo-gh, ihi+gh)), so every kernel indexes with global vertex numbers.
+// nb > 1 allocates nb consecutive blocks of stride L.B (stacked vectors).
+static double* lvec(okg_ctx* c, const Level& L, int l, int nb = 1) {
+  double* base = dalloc(c, L.B * nb);
+  double* g = base + (ptrdiff_t)L.gh * L.g.ps - (ptrdiff_t)L.g.ilo * L.g.ps;
+  for (int q = 0; q < nb; ++q) c->reg.push_back({g + (ptrdiff_t)q * L.B, l});
+  return g;
 }
 
 static void note(okg_ctx* c) {
@@ -179,15 +209,142 @@ static void launch(okg_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, 
 }
 
 static unsigned nblk(size_t n) { return static_cast<unsigned>((n + BS - 1) / BS); }
+// CTAs for one thread per owned vertex of a grid
+static unsigned own(const Grid& g) { return std::max(1u, nblk((size_t)(g.hi - g.lo))); }
 static unsigned vblk(size_t n) { return static_cast<unsigned>(std::min<size_t>((n + BS - 1) / BS, 148 * 8)); }
 
 static Reduce red(okg_ctx* c, int off) { return Reduce{c->partials, c->ticket, c->dred + off}; }
 // layout of dred
-enum { R_H = 0, R_C = 40, R_NRM = 80, R_RES = 90, R_JRES = 95, R_DOT = 100 };
+enum { R_H = 0, R_C = 40, R_NRM = 80, R_RES = 90, R_JRES = 95, R_DOT = 100, R_FLAG = 105 };
 
 static void sync_read(okg_ctx* c, int off, int cnt) {
   CK(cudaMemcpyAsync(c->hred + off, c->dred + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+}
+
+// flat pointer (allocation order, incl. ghost planes) of a fine-level vector
+static double* F(okg_ctx* c, double* p) { return p + c->foff; }
+static const double* F(okg_ctx* c, const double* p) { return p + c->foff; }
+
+static void set_owned(Grid& g, int ilo, int ihi) {
+  g.ilo = ilo;
+  g.ihi = ihi;
+  g.lo = (uint32_t)ilo * g.ps;
+  g.hi = (uint32_t)ihi * g.ps;
+}
+
+// ---------------------------------------------------------------------------
+// Slab group: one host thread + one stream per slab.  Ranks
+// exchange one ghost plane per neighbour before every stencil kernel and
+// allreduce their partial sums (in rank order: deterministic).  All the
+// cross-slab ordering is CUDA events + host barriers; no kernel ever waits on
+// another, so several slabs may share one GPU (the 1-GPU emulation the tests
+// use) or sit on different GPUs (peer copies over NVLink).
+// ---------------------------------------------------------------------------
+struct Group {
+  int S = 1;
+  std::vector<okg_ctx*> r;
+  std::atomic<int> count{0};
+  std::atomic<long> gen{0};
+  std::atomic<bool> abort{false};
+  std::vector<double> scratch;  // [S][256] allreduce staging
+  // worker threads
+  std::vector<std::thread> th;
+  std::mutex jm;
+  std::condition_variable jcv, dcv;
+  std::function<void(int)> job;
+  long jgen = 0;
+  int done = 0;
+  bool stop = false;
+  std::vector<int> status;
+
+  void barrier() {
+    const long g = gen.load(std::memory_order_acquire);
+    if (count.fetch_add(1, std::memory_order_acq_rel) + 1 == S) {
+      count.store(0, std::memory_order_relaxed);
+      gen.fetch_add(1, std::memory_order_acq_rel);
+    } else {
+      int spins = 0;
+      while (gen.load(std::memory_order_acquire) == g) {
+        if (abort.load(std::memory_order_relaxed)) THROW(OKG_EOTHER, "slab group aborted by another slab's error");
+        if (++spins > 64) std::this_thread::yield();
+      }
+    }
+  }
+};
+
+static void allreduce(okg_ctx* c, int off, int cnt) {
+  Group* G = c->group;
+  if (!G || G->S == 1) return;
+  for (int i = 0; i < cnt; ++i) G->scratch[(size_t)c->rank * 256 + i] = c->hred[off + i];
+  G->barrier();
+  for (int i = 0; i < cnt; ++i) {
+    double s = 0.0;
+    for (int q = 0; q < G->S; ++q) s += G->scratch[(size_t)q * 256 + i];
+    c->hred[off + i] = s;
+  }
+  G->barrier();
+}
+
+// hred -> dred for kernels that consume reduction results on the device
+static void write_red(okg_ctx* c, int off, int cnt) {
+  CK(cudaMemcpyAsync(c->dred + off, c->hred + off, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+}
+
+static int reg_index(okg_ctx* c, const double* x, int l) {
+  for (size_t q = 0; q < c->reg.size(); ++q)
+    if (c->reg[q].first == x && c->reg[q].second == l) return (int)q;
+  THROW(OKG_EOTHER, "exchange: vector %p (level %d) is not a registered slab vector", (const void*)x, l);
+}
+
+// refresh the ghost planes of level-l vector x from the neighbouring slabs
+static void exchange(okg_ctx* c, int l, const double* x) {
+  Group* G = c->group;
+  if (!G || G->S == 1) return;
+  const Level& L = c->lv[l];
+  if (L.gh == 0) return;
+  const int q = reg_index(c, x, l);
+  const size_t pb = (size_t)L.g.ps * sizeof(double);
+  CK(cudaEventRecord(c->ev_a, c->stream));
+  G->barrier();
+  for (int nb : {c->rank - 1, c->rank + 1}) {
+    if (nb < 0 || nb >= G->S) continue;
+    okg_ctx* o = G->r[nb];
+    CK(cudaStreamWaitEvent(c->stream, o->ev_a, 0));
+    const int plane = nb < c->rank ? L.g.ilo - 1 : L.g.ihi;
+    double* dst = const_cast<double*>(x) + (ptrdiff_t)plane * L.g.ps;
+    const double* src = o->reg[q].first + (ptrdiff_t)plane * L.g.ps;
+    CK(cudaMemcpyPeerAsync(dst, c->p.device, src, o->p.device, pb, c->stream));
+  }
+  CK(cudaEventRecord(c->ev_b, c->stream));
+  G->barrier();
+  for (int nb : {c->rank - 1, c->rank + 1})
+    if (nb >= 0 && nb < G->S) CK(cudaStreamWaitEvent(c->stream, G->r[nb]->ev_b, 0));
+}
+
+// replicated level l: every slab computed the planes of its restriction range;
+// copy them to all other slabs
+static void allgather_planes(okg_ctx* c, int l, double* x) {
+  Group* G = c->group;
+  if (!G || G->S == 1) return;
+  const int q = reg_index(c, x, l);
+  const Level& L = c->lv[l];
+  CK(cudaEventRecord(c->ev_a, c->stream));
+  G->barrier();
+  for (int o = 0; o < G->S; ++o) {
+    if (o == c->rank) continue;
+    okg_ctx* oc = G->r[o];
+    const Grid& fo = oc->lv[l - 1].g;  // the other slab's finer-level planes
+    const int a = (fo.ilo + 1) / 2, b = (fo.ihi + 1) / 2;
+    if (b <= a) continue;
+    CK(cudaStreamWaitEvent(c->stream, oc->ev_a, 0));
+    CK(cudaMemcpyPeerAsync(x + (ptrdiff_t)a * L.g.ps, c->p.device, oc->reg[q].first + (ptrdiff_t)a * L.g.ps,
+                           oc->p.device, (size_t)(b - a) * L.g.ps * sizeof(double), c->stream));
+  }
+  CK(cudaEventRecord(c->ev_b, c->stream));
+  G->barrier();
+  for (int o = 0; o < G->S; ++o)
+    if (o != c->rank) CK(cudaStreamWaitEvent(c->stream, G->r[o]->ev_b, 0));
 }
 
 static Grid make_grid(int dim, int n) {
@@ -196,6 +353,10 @@ static Grid make_grid(int dim, int n) {
   g.s = n + 1;
   g.ps = dim == 2 ? (uint32_t)g.s : (uint32_t)g.s * (uint32_t)g.s;
   g.N = dim == 2 ? g.ps * (uint32_t)g.s : g.ps * (uint32_t)g.s;
+  g.ilo = 0;
+  g.ihi = g.s;
+  g.lo = 0;
+  g.hi = g.N;
   const int noff = dim == 2 ? 7 : 15;
   for (int o = 0; o < 15; ++o) {
     if (o >= noff) {
@@ -251,17 +412,17 @@ static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const
                      double* y, double* acc, double omega = 0.0) {
   const Op<DIM> o = dev_op<DIM>(op);
   switch (epi) {
-    case EPI_APPLY: launch(c, k_op<DIM, EPI_APPLY>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega); break;
-    case EPI_RESID: launch(c, k_op<DIM, EPI_RESID>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega); break;
-    case EPI_JACOBI: launch(c, k_op<DIM, EPI_JACOBI>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega); break;
+    case EPI_APPLY: launch(c, k_op<DIM, EPI_APPLY>, own(g), BS, 0, g, o, x, b, y, acc, omega); break;
+    case EPI_RESID: launch(c, k_op<DIM, EPI_RESID>, own(g), BS, 0, g, o, x, b, y, acc, omega); break;
+    case EPI_JACOBI: launch(c, k_op<DIM, EPI_JACOBI>, own(g), BS, 0, g, o, x, b, y, acc, omega); break;
     case EPI_JACOBI_SET:
-      launch(c, k_op<DIM, EPI_JACOBI_SET>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega);
+      launch(c, k_op<DIM, EPI_JACOBI_SET>, own(g), BS, 0, g, o, x, b, y, acc, omega);
       break;
     case EPI_JACOBI_ACC:
-      launch(c, k_op<DIM, EPI_JACOBI_ACC>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega);
+      launch(c, k_op<DIM, EPI_JACOBI_ACC>, own(g), BS, 0, g, o, x, b, y, acc, omega);
       break;
     case EPI_SCALE_APPLY:
-      launch(c, k_op<DIM, EPI_SCALE_APPLY>, nblk(g.N), BS, 0, g, o, x, b, y, acc, omega);
+      launch(c, k_op<DIM, EPI_SCALE_APPLY>, own(g), BS, 0, g, o, x, b, y, acc, omega);
       break;
   }
   note(c);
@@ -306,24 +467,28 @@ static void make_tiling(okg_ctx* c, Level& L) {
   Tiling& t = L.tl;
   t.ktiles = (n - 1 + TC::TK - 1) / TC::TK;
   t.jtiles = DIM == 3 ? (n - 1 + TC::TJ - 1) / TC::TJ : 1;
+  // interior planes of this slab
+  t.ci0 = std::max(1, L.g.ilo);
+  t.ci1 = std::min(n, L.g.ihi);
+  const int nci = std::max(0, t.ci1 - t.ci0);
   const int base = t.ktiles * t.jtiles;
   // vertices per thread along x (TI): 3D 4 (register budget for 6 CTAs/SM), 2D 8;
   // smaller when the level is too small to give each SM a few CTAs
   int ichunk = DIM == 3 ? 4 : 8;
-  while (ichunk > 2 && base * ((n - 1 + ichunk - 1) / ichunk) < 148 * 4) ichunk /= 2;
-  const int nchunks = (n - 1 + ichunk - 1) / ichunk;
+  while (ichunk > 2 && base * ((nci + ichunk - 1) / ichunk) < 148 * 4) ichunk /= 2;
+  const int nchunks = (nci + ichunk - 1) / ichunk;
   t.ichunk = ichunk;
   t.ncore = base * nchunks;
   std::vector<uint32_t> bnd;
   const int s = n + 1;
   if (DIM == 3) {
-    for (int i = 0; i < s; ++i)
+    for (int i = L.g.ilo; i < L.g.ihi; ++i)
       for (int j = 0; j < s; ++j)
         for (int k = 0; k < s; ++k)
           if (i == 0 || i == n || j == 0 || j == n || k == 0 || k == n)
             bnd.push_back((uint32_t)((i * s + j) * s + k));
   } else {
-    for (int i = 0; i < s; ++i)
+    for (int i = L.g.ilo; i < L.g.ihi; ++i)
       for (int k = 0; k < s; ++k)
         if (i == 0 || i == n || k == 0 || k == n) bnd.push_back((uint32_t)(i * s + k));
   }
@@ -421,7 +586,7 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
       coarse_solve<DIM>(c, rhs, out);
     } else {
       coarse_solve<DIM>(c, rhs, L.ea);
-      axpy(c, 1.0, L.ea, out, L.g.N);
+      axpy(c, 1.0, L.ea + L.g.lo, out + L.g.lo, L.g.hi - L.g.lo);
     }
     return;
   }
@@ -437,36 +602,48 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   const int pre = c->p.mg_pre, post = c->p.mg_post;
   // ---- pre-smoothing from zero (multigrid.hpp:102-104)
   if (pre == 0) {
-    CK(cudaMemsetAsync(cur, 0, L.g.N * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(cur + L.g.lo, 0, (L.g.hi - L.g.lo) * sizeof(double), c->stream));
   } else if (pre >= 2) {
+    exchange(c, l, rhs);
     if (L.tiled) tiled<DIM, L_JAC0, T_JACOBI>(c, L, L.shat, targs(rhs, rhs, cur, nullptr, om));
     else {
-      launch(c, k_pre2<DIM>, nblk(L.g.N), BS, 0, L.g, op, rhs, cur, om);
+      launch(c, k_pre2<DIM>, own(L.g), BS, 0, L.g, op, rhs, cur, om);
       note(c);
     }
     for (int s = 2; s < pre; ++s) {
+      exchange(c, l, cur);
       if (L.tiled) tiled<DIM, L_PLAIN, T_JACOBI>(c, L, L.shat, targs(cur, rhs, oth, nullptr, om));
       else op_apply<DIM>(c, L.g, L.shat, EPI_JACOBI, cur, rhs, oth, nullptr, om);
       std::swap(cur, oth);
     }
   } else {
-    launch(c, k_jacobi0<DIM>, nblk(L.g.N), BS, 0, L.g, op, rhs, cur, om);
+    launch(c, k_jacobi0<DIM>, own(L.g), BS, 0, L.g, op, rhs, cur, om);
     note(c);
   }
   // ---- residual, restriction, coarse correction (multigrid.hpp:106-110)
+  exchange(c, l, cur);
   if (L.tiled) tiled<DIM, L_PLAIN, T_RESID>(c, L, L.shat, targs(cur, rhs, L.res, nullptr, 0.0));
   else op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
   Level& C = c->lv[l + 1];
-  launch(c, k_restrict<DIM>, nblk(C.g.N), BS, 0, L.g, C.g, L.res, C.b);
-  note(c);
+  exchange(c, l, L.res);
+  {
+    // coarse vertices G with 2G in this slab's planes (all of them when not split)
+    Grid gcr = C.g;
+    if (C.rep && !L.rep) set_owned(gcr, (L.g.ilo + 1) / 2, (L.g.ihi + 1) / 2);
+    launch(c, k_restrict<DIM>, own(gcr), BS, 0, L.g, gcr, (const double*)L.res, C.b);
+    note(c);
+    if (C.rep && !L.rep) allgather_planes(c, l + 1, C.b);
+  }
   mg_level<DIM>(c, l + 1, C.b, C.x, false);
   // ---- prolongation + post-smoothing (multigrid.hpp:111-115)
+  exchange(c, l + 1, C.x);
   if (post == 0 || !L.tiled) {
-    launch(c, k_prolong_add<DIM>, nblk(L.g.N), BS, 0, L.g, C.g, C.x, cur);
+    launch(c, k_prolong_add<DIM>, own(L.g), BS, 0, L.g, C.g, (const double*)C.x, cur);
     note(c);
   }
   for (int s = 0; s < post; ++s) {
     const bool lastsweep = (s == post - 1);
+    exchange(c, l, cur);
     if (L.tiled) {
       TArgs a = targs(cur, rhs, lastsweep ? nullptr : oth, lastsweep ? out : nullptr, om);
       if (s == 0) {  // stage e + P e_c: the correction is fused into this sweep
@@ -488,8 +665,8 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
     if (!lastsweep) std::swap(cur, oth);
   }
   if (post == 0) {
-    if (acc) axpy(c, 1.0, cur, out, L.g.N);
-    else copy(c, cur, out, L.g.N);
+    if (acc) axpy(c, 1.0, cur + L.g.lo, out + L.g.lo, L.g.hi - L.g.lo);
+    else copy(c, cur + L.g.lo, out + L.g.lo, L.g.hi - L.g.lo);
   }
 }
 
@@ -497,6 +674,7 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
 template <int DIM>
 static void apply_level(okg_ctx* c, int l, const HostOp& op, const double* x, double* y) {
   const Level& L = c->lv[l];
+  exchange(c, l, x);
   if (L.tiled) tiled<DIM, L_PLAIN, T_APPLY>(c, L, op, targs(x, nullptr, y, nullptr, 0.0));
   else op_apply<DIM>(c, L.g, op, EPI_APPLY, x, nullptr, y, nullptr);
 }
@@ -508,6 +686,7 @@ static void shat_inv(okg_ctx* c, const double* b, double* x, int cycles) {
     const double* rhs = cyc == 0 ? b : c->shr;
     mg_level<DIM>(c, 0, rhs, x, cyc > 0);
     if (cyc + 1 == cycles) break;
+    exchange(c, 0, x);
     if (c->lv[0].tiled) tiled<DIM, L_PLAIN, T_RESID>(c, c->lv[0], c->lv[0].shat, targs(x, b, c->shr, nullptr, 0.0));
     else op_apply<DIM>(c, c->lv[0].g, c->lv[0].shat, EPI_RESID, x, b, c->shr, nullptr);
   }
@@ -521,14 +700,15 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
   const int k = c->p.cheby_iters;
   double* dcur = c->cd0;
   double* dnxt = c->cd1;
-  launch(c, k_cheb_first<DIM>, nblk(g.N), BS, 0, g, o, b, dcur, c->cheb_inv_theta);
+  launch(c, k_cheb_first<DIM>, own(g), BS, 0, g, o, b, dcur, c->cheb_inv_theta);
   note(c);
   if (k == 1) {
-    copy(c, dcur, x, g.N);
+    copy(c, dcur + g.lo, x + g.lo, g.hi - g.lo);
     return;
   }
   for (int j = 0; j + 1 < k; ++j) {
     const int last = (j == k - 2);
+    exchange(c, 0, dcur);
     if (c->lv[0].tiled) {
       TArgs a = targs(dcur, j == 0 ? b : c->cr, c->cr, x, 0.0);
       a.x2 = j == 0 ? dcur : x;
@@ -538,7 +718,7 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
       a.last = last;
       tiled<DIM, L_PLAIN, T_CHEB>(c, c->lv[0], A, a);
     } else {
-      launch(c, k_cheb_step<DIM>, nblk(g.N), BS, 0, g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
+      launch(c, k_cheb_step<DIM>, own(g), BS, 0, g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
                                                         c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last);
       note(c);
     }
@@ -571,11 +751,13 @@ static void capply(okg_ctx* c, const double* x, const double* v, const double* b
   a.b = b;
   a.y = y;
   a.coef = c->coef;
-  a.ldc = c->N;
-  a.n2 = c->N;
+  a.ldc = c->B;
+  a.n2 = c->B;
   a.s1 = s1;
   a.s2 = 0.0;
   const Level& L0 = c->lv[0];
+  exchange(c, 0, x);
+  if (v && MODE >= CM_SCHUR) exchange(c, 0, v);
   if (L0.tiled) {
     CTArgs t;
     t.x = x;
@@ -583,15 +765,15 @@ static void capply(okg_ctx* c, const double* x, const double* v, const double* b
     t.b = b;
     t.y = y;
     t.coef = c->coef;
-    t.ldc = c->N;
-    t.n2 = c->N;
+    t.ldc = c->B;
+    t.n2 = c->B;
     t.s1 = s1;
     if (L0.tl.ichunk == 8) tiled_c<DIM, MODE, 8>(c, t, rd);
     else if (L0.tl.ichunk == 4) tiled_c<DIM, MODE, 4>(c, t, rd);
     else tiled_c<DIM, MODE, 2>(c, t, rd);
     return;
   }
-  launch(c, k_capply<DIM, MODE>, nblk(c->N), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K),
+  launch(c, k_capply<DIM, MODE>, own(c->fine), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K),
                                                         dev_op<DIM>(c->A), a, rd);
   note(c);
 }
@@ -621,7 +803,7 @@ static void s_inv_approx(okg_ctx* c, const double* b, double* x) {
   for (int j = 1; j < k; ++j) {
     apply_schur<DIM>(c, x, b, c->rr);
     schur_tilde_inv<DIM>(c, c->rr, c->z2);
-    axpy(c, 1.0, c->z2, x, c->N);
+    axpy(c, 1.0, c->z2 + c->fine.lo, x + c->fine.lo, c->fine.hi - c->fine.lo);
   }
 }
 
@@ -629,13 +811,13 @@ static void s_inv_approx(okg_ctx* c, const double* b, double* x) {
 template <int DIM>
 static void apply_block(okg_ctx* c, const double* p, double* z) {
   cheb<DIM>(c, c->A, p, z);
-  capply<DIM, CM_SUB>(c, z, nullptr, p + c->N, c->r2p, 0.0);
-  s_inv_approx<DIM>(c, c->r2p, z + c->N);
+  capply<DIM, CM_SUB>(c, z, nullptr, p + c->B, c->r2p, 0.0);
+  s_inv_approx<DIM>(c, c->r2p, z + c->B);
 }
 
 template <int DIM>
 static void jacobian(okg_ctx* c, const double* x, double* y) {
-  capply<DIM, CM_JAC>(c, x, x + c->N, nullptr, y, c->dt_theta);
+  capply<DIM, CM_JAC>(c, x, x + c->B, nullptr, y, c->dt_theta);
 }
 
 static void check_lin(okg_ctx* c, const char* what) {
@@ -708,10 +890,12 @@ static double residual(okg_ctx* c, const double* un, const double* wn, const dou
   a.eps2 = c->p.eps * c->p.eps;
   a.b_int = c->b_int;
   a.b_tab = c->b_tab;
-  launch(c, k_residual<DIM>, nblk(c->N), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K), c->nl, a,
+  for (const double* v : {un, wn, uo, wo}) exchange(c, 0, v);
+  launch(c, k_residual<DIM>, own(c->fine), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K), c->nl, a,
                                                    red(c, R_RES));
   note(c);
   sync_read(c, R_RES, 2);
+  allreduce(c, R_RES, 2);
   const double na = std::sqrt(c->hred[R_RES]), nb = std::sqrt(c->hred[R_RES + 1]);
   if (s1out) *s1out = c->hred[R_RES] + c->hred[R_RES + 1];
   return std::sqrt(na * na + nb * nb);  // stacked_norm, model.hpp:152-155
@@ -719,9 +903,12 @@ static double residual(okg_ctx* c, const double* un, const double* wn, const dou
 
 template <int DIM>
 static void linearize(okg_ctx* c, const double* u) {
-  launch(c, k_linearize<DIM>, nblk(c->N), BS, 0, c->fine, dev_op<DIM>(c->K), c->nl, c->p.eps * c->p.eps, u,
-                                                    c->coef, c->N);
+  exchange(c, 0, u);
+  launch(c, k_linearize<DIM>, own(c->fine), BS, 0, c->fine, dev_op<DIM>(c->K), c->nl, c->p.eps * c->p.eps, u,
+                                                    c->coef, c->B);
   note(c);
+  // the negative stencil slots of C are read at the neighbour (positive arrays q >= 1)
+  for (int q = 1; q <= Traits<DIM>::NPOS; ++q) exchange(c, 0, c->coef + (ptrdiff_t)q * c->B);
   c->have_lin = true;
 }
 
@@ -732,46 +919,73 @@ static void givens(double cs, double sn, double& a, double& b) {
   a = t;
 }
 
+// CGS2: h = V^T w (+ ||w||^2), w' = w - V h, c = V^T w', w'' = w' - V c, ||w''||^2.
+// With several slabs every partial reduction is allreduced before a kernel
+// consumes it (the single-slab path reads the sums straight from device memory).
 template <int NVB>
 static void arnoldi_ortho(okg_ctx* c, int nv) {
-  const size_t n2 = c->N2;
-  launch(c, k_arnoldi_dot<NVB>, vblk(n2), BS, 0, nv, c->pw, c->V, n2, n2, red(c, R_H));
+  const size_t n2 = c->N2, ne = 2 * c->seg.len;
+  double* pw = F(c, c->pw);
+  double* gt = F(c, c->gt);
+  launch(c, k_arnoldi_dot<NVB>, vblk(ne), BS, 0, nv, (const double*)pw, (const double*)c->V, n2, c->seg, ne,
+         red(c, R_H));
   note(c);
-  // put ||w||^2 after the h values at a fixed slot
-  launch(c, k_arnoldi_update<NVB, 0>, vblk(n2), BS, 0, nv, c->pw, c->V, n2, n2, c->dred + R_H, c->gt,
-                                                           red(c, R_C));
+  if (c->nslabs > 1) {
+    sync_read(c, R_H, NVB + 1);
+    allreduce(c, R_H, NVB + 1);
+    write_red(c, R_H, NVB + 1);
+  }
+  launch(c, k_arnoldi_update<NVB, 0>, vblk(ne), BS, 0, nv, (const double*)pw, (const double*)c->V, n2, c->seg, ne,
+         (const double*)(c->dred + R_H), gt, red(c, R_C));
   note(c);
-  launch(c, k_arnoldi_update<NVB, 1>, vblk(n2), BS, 0, nv, c->gt, c->V, n2, n2, c->dred + R_C, c->pw,
-                                                           red(c, R_NRM));
+  if (c->nslabs > 1) {
+    sync_read(c, R_C, NVB);
+    allreduce(c, R_C, NVB);
+    write_red(c, R_C, NVB);
+  }
+  launch(c, k_arnoldi_update<NVB, 1>, vblk(ne), BS, 0, nv, (const double*)gt, (const double*)c->V, n2, c->seg, ne,
+         (const double*)(c->dred + R_C), pw, red(c, R_NRM));
   note(c);
+  if (c->nslabs > 1) {
+    sync_read(c, R_NRM, 1);
+    allreduce(c, R_NRM, 1);
+    write_red(c, R_NRM, 1);
+  }
 }
 
 // generic (nv > 32): chunked classical Gram-Schmidt twice
 static void arnoldi_ortho_chunked(okg_ctx* c, int nv, std::vector<double>& hsum, double& ww) {
-  const size_t n2 = c->N2;
+  const size_t n2 = c->N2, ne = 2 * c->seg.len;
+  double* pw = F(c, c->pw);
+  double* gt = F(c, c->gt);
   hsum.assign(nv, 0.0);
   for (int pass = 0; pass < 2; ++pass) {
     std::vector<double> hh(nv, 0.0);
     for (int q0 = 0; q0 < nv; q0 += 32) {
       const int cnt = std::min(32, nv - q0);
-      launch(c, k_arnoldi_dot<32>, vblk(n2), BS, 0, cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2, red(c, R_H));
+      launch(c, k_arnoldi_dot<32>, vblk(ne), BS, 0, cnt, (const double*)pw, (const double*)(c->V + (size_t)q0 * n2),
+             n2, c->seg, ne, red(c, R_H));
       note(c);
       sync_read(c, R_H, 33);
+      allreduce(c, R_H, 33);
       for (int q = 0; q < cnt; ++q) hh[q0 + q] = c->hred[R_H + q];
       if (pass == 0 && q0 == 0) ww = c->hred[R_H + 32];
     }
     for (int q0 = 0; q0 < nv; q0 += 32) {
       const int cnt = std::min(32, nv - q0);
       CK(cudaMemcpyAsync(c->dred + R_C, hh.data() + q0, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      launch(c, k_arnoldi_update<32, 1>, vblk(n2), BS, 0, cnt, c->pw, c->V + (size_t)q0 * n2, n2, n2,
-                                                             c->dred + R_C, c->gt, red(c, R_NRM));
+      launch(c, k_arnoldi_update<32, 1>, vblk(ne), BS, 0, cnt, (const double*)pw,
+             (const double*)(c->V + (size_t)q0 * n2), n2, c->seg, ne, (const double*)(c->dred + R_C), gt,
+             red(c, R_NRM));
       note(c);
-      copy(c, c->gt, c->pw, n2);
+      copy(c, gt, pw, n2);
       CK(cudaStreamSynchronize(c->stream));
     }
     for (int q = 0; q < nv; ++q) hsum[q] += hh[q];
   }
   sync_read(c, R_NRM, 1);
+  allreduce(c, R_NRM, 1);
+  write_red(c, R_NRM, 1);
 }
 
 template <int DIM>
@@ -785,12 +999,14 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
     if (st->n_residual_norms < 512) st->residual_norms[st->n_residual_norms] = v;
     st->n_residual_norms++;
   };
-  CK(cudaMemsetAsync(x, 0, n2 * sizeof(double), c->stream));
+  const size_t ne = 2 * c->seg.len;
+  CK(cudaMemsetAsync(F(c, x), 0, n2 * sizeof(double), c->stream));
   double nb2 = norm_b_sq;
   if (nb2 < 0.0) {
-    launch(c, k_dot, vblk(n2), BS, 0, b, b, n2, red(c, R_DOT));
+    launch(c, k_dot, vblk(ne), BS, 0, (const double*)F(c, b), (const double*)F(c, b), c->seg, ne, red(c, R_DOT));
     note(c);
     sync_read(c, R_DOT, 1);
+    allreduce(c, R_DOT, 1);
     nb2 = c->hred[R_DOT];
   }
   // require_finite(b) (krylov.hpp:52): any NaN/Inf entry makes the sum of squares non-finite
@@ -810,9 +1026,9 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
   std::vector<double> cs, sn, g, hsum;
   while (st->iterations < max_iter) {
     // V0 = r / beta
-    launch(c, k_scale, vblk(n2), BS, 0, 1.0 / beta, r, c->V, n2);
+    launch(c, k_scale, vblk(n2), BS, 0, 1.0 / beta, (const double*)F(c, r), c->V, n2);
     note(c);
-    copy(c, c->V, c->pin, n2);
+    copy(c, c->V, F(c, c->pin), n2);
     H.clear();
     cs.clear();
     sn.clear();
@@ -830,8 +1046,8 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
         else if (nv <= 16) arnoldi_ortho<16>(c, nv);
         else arnoldi_ortho<32>(c, nv);
         // V_{j+1} = w / ||w||  (speculative; unused on exit)
-        launch(c, k_normalize, vblk(n2), BS, 0, c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
-                                                     n2);
+        launch(c, k_normalize, vblk(n2), BS, 0, (const double*)F(c, c->pw), (const double*)(c->dred + R_NRM),
+               c->V + (size_t)(j + 1) * n2, F(c, c->pin), n2);
         note(c);
         const int nvb = nv <= 4 ? 4 : nv <= 8 ? 8 : nv <= 16 ? 16 : 32;
         // dred[R_H + nvb] holds ||w||^2 (slot NVB of the first reduction)
@@ -844,8 +1060,8 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
         arnoldi_ortho_chunked(c, nv, hsum, ww);
         for (int q = 0; q < nv; ++q) h[q] = hsum[q];
         arnoldi_norm = std::sqrt(c->hred[R_NRM]);
-        launch(c, k_normalize, vblk(n2), BS, 0, c->pw, c->dred + R_NRM, c->V + (size_t)(j + 1) * n2, c->pin,
-                                                     n2);
+        launch(c, k_normalize, vblk(n2), BS, 0, (const double*)F(c, c->pw), (const double*)(c->dred + R_NRM),
+               c->V + (size_t)(j + 1) * n2, F(c, c->pin), n2);
         note(c);
       }
       const double w_scale = std::sqrt(ww);
@@ -885,19 +1101,20 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
       const int cnt = std::min(32, j - q0);
       for (int q = 0; q < 32; ++q) yc.c[q] = q < cnt ? y[q0 + q] : 0.0;
       if (q0 == 0) {
-        launch(c, k_combine, vblk(n2), BS, 0, std::max(cnt, 0), yc, c->V, n2, n2, c->pin);
+        launch(c, k_combine, vblk(n2), BS, 0, std::max(cnt, 0), yc, (const double*)c->V, n2, n2, F(c, c->pin));
         note(c);
       } else {
-        launch(c, k_combine, vblk(n2), BS, 0, cnt, yc, c->V + (size_t)q0 * n2, n2, n2, c->gt);
+        launch(c, k_combine, vblk(n2), BS, 0, cnt, yc, (const double*)(c->V + (size_t)q0 * n2), n2, n2, F(c, c->gt));
         note(c);
-        axpy(c, 1.0, c->gt, c->pin, n2);
+        axpy(c, 1.0, F(c, c->gt), F(c, c->pin), n2);
       }
     }
     run_arnoldi_op<DIM>(c, false);  // pz = P^-1 u
-    axpy(c, 1.0, c->pz, x, n2);
+    axpy(c, 1.0, F(c, c->pz), F(c, x), n2);
     // r = b - J x, beta = ||r||   (krylov.hpp:135-138)
-    capply<DIM, CM_JAC_RES>(c, x, x + c->N, b, c->gr, c->dt_theta, red(c, R_JRES));
+    capply<DIM, CM_JAC_RES>(c, x, x + c->B, b, c->gr, c->dt_theta, red(c, R_JRES));
     sync_read(c, R_JRES, 1);
+    allreduce(c, R_JRES, 1);
     beta = std::sqrt(c->hred[R_JRES]);
     st->final_residual = beta;
     r = c->gr;
@@ -915,54 +1132,71 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
 }
 
 // ---- Lanczos bounds (krylov.hpp:248-320) ------------------------------------------------
+// Same start vector as the reference (std::mt19937(1234), uniform(-1,1) over
+// the GLOBAL vertex order; each slab keeps its slice); dots allreduced.
 template <int DIM>
 static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
-  const uint32_t n = c->N;
-  const int steps = (int)std::min<uint32_t>(30u, n);
+  const Level& L0 = c->lv[0];
+  const uint64_t Nglob = L0.g.N;
+  const size_t nloc = L0.g.hi - L0.g.lo, B = L0.B;
+  const int steps = (int)std::min<uint64_t>(30u, Nglob);
   std::mt19937 rng(1234u);
   std::uniform_real_distribution<double> dist(-1.0, 1.0);
-  std::vector<double> hv(n);
+  for (uint64_t g = 0; g < L0.g.lo; ++g) (void)dist(rng);
+  std::vector<double> hv(nloc);
   for (auto& e : hv) e = dist(rng);
-  std::vector<double*> Vv;
-  auto dot = [&](const double* a, const double* b) {
-    launch(c, k_dot, vblk(n), BS, 0, a, b, n, red(c, R_DOT));
+  // scratch: steps+1 level-0 blocks, in the Krylov basis when it is large enough
+  const size_t need = (size_t)steps + 1;
+  double* flat = c->V;
+  double* tmp = nullptr;
+  if ((size_t)2 * c->vcap < need) {
+    CK(cudaMalloc(&tmp, need * B * sizeof(double)));
+    CK(cudaMemsetAsync(tmp, 0, need * B * sizeof(double), c->stream));
+    flat = tmp;
+  }
+  const size_t reg0 = c->reg.size();
+  auto blk = [&](size_t q) {
+    double* g = flat + q * B - c->foff;
+    c->reg.push_back({g, 0});
+    return g;
+  };
+  const Seg s1{(size_t)L0.gh * L0.g.ps, nloc, B};
+  auto dot = [&](const double* x, const double* y) {
+    launch(c, k_dot, vblk(nloc), BS, 0, (const double*)F(c, x), (const double*)F(c, y), s1, nloc, red(c, R_DOT));
     note(c);
     sync_read(c, R_DOT, 1);
+    allreduce(c, R_DOT, 1);
     return c->hred[R_DOT];
   };
-  // basis in the Krylov buffer space (gb, gx, ... are free at setup): use V if large enough
-  std::vector<double*> own;
-  auto vec = [&]() {
-    double* p = nullptr;
-    CK(cudaMalloc(&p, n * sizeof(double)));
-    own.push_back(p);
-    return p;
-  };
-  double* v0 = vec();
-  CK(cudaMemcpyAsync(v0, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  std::vector<double*> Vv;
+  double* v0 = blk(0);
+  CK(cudaMemcpyAsync(v0 + L0.g.lo, hv.data(), nloc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   const double nv0 = std::sqrt(dot(v0, v0));
-  scale(c, 1.0 / nv0, v0, v0, n);
+  scale(c, 1.0 / nv0, F(c, v0), F(c, v0), B);
   Vv.push_back(v0);
-  double* w = vec();
+  double* w = blk(need - 1);
   std::vector<double> alpha, beta;
   for (int j = 0; j < steps; ++j) {
+    exchange(c, 0, Vv[j]);
     op_apply<DIM>(c, c->fine, c->M, EPI_SCALE_APPLY, Vv[j], nullptr, w, nullptr);
     const double a = dot(w, Vv[j]);
     alpha.push_back(a);
-    axpy(c, -a, Vv[j], w, n);
-    if (j > 0) axpy(c, -beta[j - 1], Vv[j - 1], w, n);
-    for (double* q : Vv) axpy(c, -dot(w, q), q, w, n);
+    axpy(c, -a, F(c, Vv[j]), F(c, w), B);
+    if (j > 0) axpy(c, -beta[j - 1], F(c, Vv[j - 1]), F(c, w), B);
+    for (double* q : Vv) axpy(c, -dot(w, q), F(c, q), F(c, w), B);
     const double nb = std::sqrt(dot(w, w));
     if (nb <= 1e-13 * std::abs(a) + 1e-300) break;
     if (j + 1 < steps) {
       beta.push_back(nb);
-      double* nvp = vec();
-      scale(c, 1.0 / nb, w, nvp, n);
+      double* nvp = blk(j + 1);
+      scale(c, 1.0 / nb, F(c, w), F(c, nvp), B);
       Vv.push_back(nvp);
     }
   }
   CK(cudaStreamSynchronize(c->stream));
-  for (double* p : own) cudaFree(p);
+  c->reg.resize(reg0);
+  if (tmp) cudaFree(tmp);
+  else CK(cudaMemsetAsync(c->V, 0, need * B * sizeof(double), c->stream));
   const int m = static_cast<int>(alpha.size());
   std::vector<double> T(static_cast<size_t>(m) * m, 0.0), ev;
   for (int i = 0; i < m; ++i) {
@@ -989,7 +1223,6 @@ static void build(okg_ctx* c) {
   const double hd = ipow(c->h, DIM), hk = ipow(c->h, DIM - 2);
   c->fine = make_grid(DIM, n);
   c->N = c->fine.N;
-  c->N2 = 2 * (size_t)c->N;
   c->M = make_op(c, ut, ut.M, hd, nullptr, 0.0, false);
   c->K = make_op(c, ut, ut.K, hk, nullptr, 0.0, false);
   {
@@ -1034,20 +1267,57 @@ static void build(okg_ctx* c) {
     if (coarsest > std::max<int64_t>(p.min_coarse_size, 2000))
       THROW(OKG_ECONFIG,
             "build_hierarchy: coarsest level too large for a direct solve; choose a grid with more factors of two");
+    // slab partition: whole x-planes, even boundaries on the finest
+    // level, coarse ranges by nesting (G owned iff 2G owned); from the first level
+    // where a slab would keep < 2 planes on, levels are replicated on every slab.
+    const int S = c->nslabs;
+    c->L_rep = (int)c->lv.size();
+    if (S > 1) {
+      const int s0 = c->lv[0].g.s;
+      int a = 2 * (int)(((long)c->rank * s0) / (2L * S)), b = 2 * (int)(((long)(c->rank + 1) * s0) / (2L * S));
+      if (c->rank == S - 1) b = s0;
+      for (size_t l = 0; l < c->lv.size(); ++l) {
+        // smallest slab of this level (same formula for every rank)
+        int minp = 1 << 30;
+        for (int r = 0; r < S; ++r) {
+          int ra = 2 * (int)(((long)r * s0) / (2L * S)), rb = r == S - 1 ? s0 : 2 * (int)(((long)(r + 1) * s0) / (2L * S));
+          for (size_t k = 0; k < l; ++k) {
+            ra = (ra + 1) / 2;
+            rb = (rb + 1) / 2;
+          }
+          minp = std::min(minp, rb - ra);
+        }
+        if (minp < 2 || l + 1 == c->lv.size()) {
+          c->L_rep = (int)l;
+          break;
+        }
+        set_owned(c->lv[l].g, a, b);
+        c->lv[l].gh = 1;
+        a = (a + 1) / 2;
+        b = (b + 1) / 2;
+      }
+      if (c->L_rep == 0) THROW(OKG_EINVAL, "slab decomposition: %d slabs leave fewer than 2 planes each", S);
+      for (size_t l = c->L_rep; l < c->lv.size(); ++l) c->lv[l].rep = true;
+    }
     for (size_t l = 0; l < c->lv.size(); ++l) {
       Level& L = c->lv[l];
-      const size_t nl = L.g.N;
+      L.B = (size_t)(L.g.ihi - L.g.ilo + 2 * L.gh) * L.g.ps;
       if (l > 0) {
-        L.b = dalloc(c, nl);
-        L.x = dalloc(c, nl);
+        L.b = lvec(c, L, (int)l);
+        L.x = lvec(c, L, (int)l);
       }
-      L.ea = dalloc(c, nl);
-      L.eb = dalloc(c, nl);
-      L.res = dalloc(c, nl);
+      L.ea = lvec(c, L, (int)l);
+      L.eb = lvec(c, L, (int)l);
+      L.res = lvec(c, L, (int)l);
     }
-    // single-CTA tail for the small levels (okg_tail.cuh)
+    c->fine = c->lv[0].g;
+    c->B = c->lv[0].B;
+    c->foff = ((ptrdiff_t)c->fine.ilo - c->lv[0].gh) * c->fine.ps;
+    c->seg = Seg{(size_t)c->lv[0].gh * c->fine.ps, (size_t)(c->fine.hi - c->fine.lo), c->B};
+    c->N2 = 2 * c->B;
+    // single-CTA tail for the small levels (okg_tail.cuh); single slab only
     const int64_t tmax = p.tail_max_vertices;
-    if (tmax > 0) {
+    if (tmax > 0 && S == 1) {
       for (size_t l = 1; l < c->lv.size(); ++l)
         if ((int64_t)c->lv[l].g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL) {
           c->tail_start = (int)l;
@@ -1057,9 +1327,12 @@ static void build(okg_ctx* c) {
     // temporally blocked down/up kernels for V(2,2) (okg_vcycle.cuh)
     // default: every coarse level in 2D; in 3D the levels with n <= 32 (the halo-3
     // redundancy of a 3D box outweighs the saved launches on bigger levels)
+    // (halo 3 / 2: only on levels that are not split across slabs)
     if (p.mg_pre == 2 && p.mg_post == 2 && p.mg_fuse >= 0)
       for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l)
-        if (p.mg_fuse == 1 || DIM == 2 || c->lv[l].g.n <= 32) c->lv[l].fused = true;
+        if ((p.mg_fuse == 1 || DIM == 2 || c->lv[l].g.n <= 32) && c->lv[l].gh == 0 &&
+            (c->lv[l].rep || S == 1))
+          c->lv[l].fused = true;
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
     const int tmin = p.tiled_min_n == 0 ? (DIM == 3 ? 32 : 128) : p.tiled_min_n;
     if (tmin > 0)
@@ -1099,8 +1372,9 @@ static void build(okg_ctx* c) {
     CK(cudaMemcpyAsync(c->Ainv, Ai.data(), Ai.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   }
   // buffers
-  const size_t N = c->N, N2 = c->N2;
-  c->max_blocks = std::max<size_t>(nblk(N), 148 * 8) + 1;
+  const size_t N2 = c->N2;
+  Level& L0 = c->lv[0];
+  c->max_blocks = std::max<size_t>(nblk(c->N), 148 * 8) + 1;
   c->partials = dalloc(c, c->max_blocks * 40);
   {
     void* t = nullptr;
@@ -1112,20 +1386,14 @@ static void build(okg_ctx* c) {
   }
   c->dred = dalloc(c, 256);
   CK(cudaMallocHost(&c->hred, 256 * sizeof(double)));
-  c->coef = dalloc(c, (size_t)(Traits<DIM>::NPOS + 1) * N);
+  c->coef = lvec(c, L0, 0, Traits<DIM>::NPOS + 1);
   const int cycle_len = p.gmres_restart > 0 ? std::min(p.gmres_restart, p.gmres_maxit) : p.gmres_maxit;
   c->vcap = cycle_len + 1;
   c->V = dalloc(c, (size_t)c->vcap * N2);
-  c->gb = dalloc(c, N2);
-  c->gx = dalloc(c, N2);
-  c->gr = dalloc(c, N2);
-  c->pin = dalloc(c, N2);
-  c->pz = dalloc(c, N2);
-  c->pw = dalloc(c, N2);
-  c->gt = dalloc(c, N2);
+  for (double** b : {&c->gb, &c->gx, &c->gr, &c->pin, &c->pz, &c->pw, &c->gt}) *b = lvec(c, L0, 0, 2);
   for (double** b : {&c->cd0, &c->cd1, &c->cr, &c->r2p, &c->sy, &c->st, &c->kv, &c->zz, &c->rr, &c->z2, &c->shr,
                      &c->u_old, &c->w_old, &c->u, &c->w})
-    *b = dalloc(c, N);
+    *b = lvec(c, L0, 0);
   // Chebyshev bounds and coefficients
   jacobi_spectrum<DIM>(c, c->lambda_lo, c->lambda_hi);
   {
@@ -1183,12 +1451,12 @@ static void newton_step_impl(okg_ctx* c, okg_step_stats* stats) {
   okg_step_stats st;
   std::memset(&st, 0, sizeof st);
   const okg_params& p = c->p;
-  const size_t N = c->N;
-  copy(c, c->u_old, c->u, N);
-  copy(c, c->w_old, c->w, N);
+  const size_t B = c->B;
+  copy(c, F(c, c->u_old), F(c, c->u), B);
+  copy(c, F(c, c->w_old), F(c, c->w), B);
   double s2 = 0.0;
   // residual(next, old) with next = old; gb = -[R1; R2]  (model.hpp:178, :187-190)
-  double rnorm = residual<DIM>(c, c->u, c->w, c->u_old, c->w_old, c->gb, c->gb + N, -1.0, &s2);
+  double rnorm = residual<DIM>(c, c->u, c->w, c->u_old, c->w_old, c->gb, c->gb + B, -1.0, &s2);
   const double ref = std::max(1.0, rnorm);
   bool done = rnorm <= p.newton_tol * ref;
   while (!done && st.newton_iters < p.newton_maxit) {
@@ -1198,19 +1466,22 @@ static void newton_step_impl(okg_ctx* c, okg_step_stats* stats) {
     if (st.newton_iters < OKG_MAX_NEWTON) st.gmres_iters[st.newton_iters] = ks.iterations;
     // require_finite(lin.x) (model.hpp:196)
     CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
-    launch(c, k_check_finite, vblk(c->N2), BS, 0, c->gx, c->N2, c->dflag);
+    launch(c, k_check_finite, vblk(2 * c->seg.len), BS, 0, (const double*)F(c, c->gx), c->seg, 2 * c->seg.len,
+           c->dflag);
     note(c);
     int flag = 0;
     CK(cudaMemcpyAsync(&flag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (flag) {
+    c->hred[R_FLAG] = flag ? 1.0 : 0.0;
+    allreduce(c, R_FLAG, 1);
+    if (c->hred[R_FLAG] != 0.0) {
       c->have_lin = false;
       THROW(OKG_EINVAL, "newton update: vector contains NaN/Inf");
     }
-    axpy(c, 1.0, c->gx, c->u, N);
-    axpy(c, 1.0, c->gx + N, c->w, N);
+    axpy(c, 1.0, F(c, c->gx), F(c, c->u), B);
+    axpy(c, 1.0, F(c, c->gx) + B, F(c, c->w), B);
     ++st.newton_iters;
-    rnorm = residual<DIM>(c, c->u, c->w, c->u_old, c->w_old, c->gb, c->gb + N, -1.0, &s2);
+    rnorm = residual<DIM>(c, c->u, c->w, c->u_old, c->w_old, c->gb, c->gb + B, -1.0, &s2);
     done = rnorm <= p.newton_tol * ref;
   }
   c->have_lin = false;  // ctx.Me = nullptr (model.hpp:207)

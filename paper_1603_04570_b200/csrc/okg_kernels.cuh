@@ -110,8 +110,8 @@ __global__ void __launch_bounds__(BS) k_op(Grid g, Op<DIM> op, const double* __r
                                            const double* __restrict__ b, double* __restrict__ y,
                                            double* __restrict__ acc, double omega) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   if (EPI == EPI_SCALE_APPLY) {
     // t_j = x_j / sqrt(d_j); y_i = (sum_j A_ij t_j) / sqrt(d_i)
@@ -150,8 +150,8 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_jacobi0(Grid g, Op<DIM> op, const double* __restrict__ b,
                                                 double* __restrict__ x, double omega) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   x[idx] = omega * op_invd<DIM>(op, nd.cls) * b[idx];
 }
@@ -163,8 +163,8 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_pre2(Grid g, Op<DIM> op, const double* __restrict__ r,
                                              double* __restrict__ e, double omega) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   constexpr int NO = Traits<DIM>::NOFF;
   double s = 0.0;
@@ -199,8 +199,8 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
                                                  double* __restrict__ rc) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= gc.N) return;
+  const uint32_t idx = gc.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= gc.hi) return;
   const Node<DIM> nc = locate<DIM>(gc, idx);
   const uint32_t F = (DIM == 3) ? (uint32_t)(2 * nc.i) * gf.ps + (uint32_t)(2 * nc.j) * gf.s + 2 * nc.k
                                 : (uint32_t)(2 * nc.i) * gf.s + 2 * nc.j;
@@ -224,8 +224,8 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_prolong_add(Grid gf, Grid gc, const double* __restrict__ ec,
                                                     double* __restrict__ x) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= gf.N) return;
+  const uint32_t idx = gf.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= gf.hi) return;
   const Node<DIM> nd = locate<DIM>(gf, idx);
   const int li = nd.i >> 1, lj = nd.j >> 1, lk = nd.k >> 1;
   const int hi = (nd.i + 1) >> 1, hj = (nd.j + 1) >> 1, hk = (nd.k + 1) >> 1;
@@ -267,8 +267,8 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_cheb_first(Grid g, Op<DIM> A, const double* __restrict__ r,
                                                    double* __restrict__ d, double inv_theta) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   d[idx] = (r[idx] * op_invd<DIM>(A, nd.cls)) * inv_theta;
 }
@@ -279,8 +279,8 @@ __global__ void __launch_bounds__(BS) k_cheb_step(Grid g, Op<DIM> A, const doubl
                                                   double* __restrict__ d_out, double* r_out, double* x_out,
                                                   double c1, double c2, int last) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   const double ad = op_row<DIM>(A, g, idx, nd.cls, [&](uint32_t j) { return __ldg(d + j); });
   const double r = r_in[idx] - ad;
@@ -391,8 +391,8 @@ __global__ void __launch_bounds__(BS) k_linearize(Grid g, Op<DIM> Kop, Nonlin nl
                                                   const double* __restrict__ u, double* __restrict__ coef,
                                                   size_t ldc) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   constexpr int NO = Traits<DIM>::NOFF, C = Traits<DIM>::CENTER, NP = Traits<DIM>::NPOS;
   double ul[NO];
@@ -449,9 +449,9 @@ template <int DIM, int MODE>
 __global__ void __launch_bounds__(BS) k_capply(Grid g, Op<DIM> Mop, Op<DIM> Kop, Op<DIM> Aop, CArgs a,
                                                Reduce red) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
   double nrm[1] = {0.0};
-  if (idx < g.N) {
+  if (idx < g.hi) {
     const Node<DIM> nd = locate<DIM>(g, idx);
     auto ldx = [&](uint32_t j) { return __ldg(a.x + j); };
     if (MODE == CM_C || MODE == CM_SUB || MODE == CM_ME) {
@@ -527,9 +527,9 @@ __global__ void __launch_bounds__(BS) k_residual(Grid g, Op<DIM> Mop, Op<DIM> Ko
                                                  Reduce red) {
   PDL_ENTRY();
   constexpr int NO = Traits<DIM>::NOFF;
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
   double v[2] = {0.0, 0.0};
-  if (idx < g.N) {
+  if (idx < g.hi) {
     const Node<DIM> nd = locate<DIM>(g, idx);
     const double bi = nd.cls == Traits<DIM>::INTERIOR ? a.b_int : __ldg(a.b_tab + nd.cls);
     double un[NO], wn[NO], uo[NO], wo[NO], du[NO];
@@ -568,8 +568,8 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_nonlinear(Grid g, Nonlin nl, const double* __restrict__ u,
                                                   double* __restrict__ y) {
   PDL_ENTRY();
-  const uint32_t idx = blockIdx.x * BS + threadIdx.x;
-  if (idx >= g.N) return;
+  const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
+  if (idx >= g.hi) return;
   const Node<DIM> nd = locate<DIM>(g, idx);
   double ul[Traits<DIM>::NOFF];
   load_ring<DIM>(g, idx, nd.cls, u, ul);
@@ -578,23 +578,32 @@ __global__ void __launch_bounds__(BS) k_nonlinear(Grid g, Nonlin nl, const doubl
 
 // ---------------------------------------------------------------------------
 // Krylov vector kernels (grid-stride, fixed grid => deterministic sums).
+// Reductions visit only the owned entries of a (possibly ghost-padded)
+// stacked vector: [off, off+len) and [B+off, B+off+len).  Unpadded: off = 0,
+// len = B = N, so the mapping is the identity.
 // ---------------------------------------------------------------------------
+struct Seg {
+  size_t off, len, B;
+};
+__device__ __forceinline__ size_t seg_flat(const Seg& s, size_t i) {
+  return i < s.len ? s.off + i : s.B + s.off + (i - s.len);
+}
 // out[q] = V_q . w (q < nv), out[NVB] = w . w
 // All basis loads of an element are issued before any FMA (the compiler
 // otherwise recycles one register and serialises them); two elements per
 // thread per iteration for more bytes in flight.
 template <int NVB>
 __global__ void __launch_bounds__(BS) k_arnoldi_dot(int nv, const double* __restrict__ w,
-                                                    const double* __restrict__ V, size_t ldv, size_t n,
+                                                    const double* __restrict__ V, size_t ldv, Seg sg, size_t n,
                                                     Reduce red) {
   PDL_ENTRY();
   double acc[NVB + 1];
 #pragma unroll
   for (int q = 0; q <= NVB; ++q) acc[q] = 0.0;
   const size_t stride = (size_t)gridDim.x * BS;
-  for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += 2 * stride) {
-    const size_t i2 = i + stride;
-    const bool two = i2 < n;
+  for (size_t ii = (size_t)blockIdx.x * BS + threadIdx.x; ii < n; ii += 2 * stride) {
+    const bool two = ii + stride < n;
+    const size_t i = seg_flat(sg, ii), i2 = two ? seg_flat(sg, ii + stride) : 0;
     double v1[NVB], v2[NVB];
 #pragma unroll
     for (int q = 0; q < NVB; ++q) {
@@ -612,7 +621,7 @@ __global__ void __launch_bounds__(BS) k_arnoldi_dot(int nv, const double* __rest
 // w_out = w - sum_q h_q V_q ; then out[q] = V_q . w_out (MODE 0) or out[0] = ||w_out||^2 (MODE 1)
 template <int NVB, int MODE>
 __global__ void __launch_bounds__(BS) k_arnoldi_update(int nv, const double* __restrict__ w,
-                                                       const double* __restrict__ V, size_t ldv, size_t n,
+                                                       const double* __restrict__ V, size_t ldv, Seg sg, size_t n,
                                                        const double* __restrict__ h, double* __restrict__ w_out,
                                                        Reduce red) {
   PDL_ENTRY();
@@ -623,7 +632,8 @@ __global__ void __launch_bounds__(BS) k_arnoldi_update(int nv, const double* __r
   double acc[NR];
 #pragma unroll
   for (int q = 0; q < NR; ++q) acc[q] = 0.0;
-  for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS) {
+  for (size_t ii = (size_t)blockIdx.x * BS + threadIdx.x; ii < n; ii += (size_t)gridDim.x * BS) {
+    const size_t i = seg_flat(sg, ii);
     double vi[NVB];
 #pragma unroll
     for (int q = 0; q < NVB; ++q) vi[q] = q < nv ? __ldg(V + q * ldv + i) : 0.0;
@@ -689,20 +699,22 @@ __global__ void __launch_bounds__(BS) k_scale(double s, const double* __restrict
 }
 
 // dot products of pairs (single value)
-__global__ void __launch_bounds__(BS) k_dot(const double* __restrict__ a, const double* __restrict__ b, size_t n,
-                                            Reduce red) {
+__global__ void __launch_bounds__(BS) k_dot(const double* __restrict__ a, const double* __restrict__ b, Seg sg,
+                                            size_t n, Reduce red) {
   PDL_ENTRY();
   double acc[1] = {0.0};
-  for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS)
+  for (size_t ii = (size_t)blockIdx.x * BS + threadIdx.x; ii < n; ii += (size_t)gridDim.x * BS) {
+    const size_t i = seg_flat(sg, ii);
     acc[0] = fma(__ldg(a + i), __ldg(b + i), acc[0]);
+  }
   grid_reduce<1>(acc, red);
 }
 
 // any non-finite entry -> *flag = 1
-__global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ x, size_t n, int* flag) {
+__global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ x, Seg sg, size_t n, int* flag) {
   PDL_ENTRY();
-  for (size_t i = (size_t)blockIdx.x * BS + threadIdx.x; i < n; i += (size_t)gridDim.x * BS)
-    if (!isfinite(x[i])) *flag = 1;
+  for (size_t ii = (size_t)blockIdx.x * BS + threadIdx.x; ii < n; ii += (size_t)gridDim.x * BS)
+    if (!isfinite(x[seg_flat(sg, ii)])) *flag = 1;
 }
 
 }  // namespace okg

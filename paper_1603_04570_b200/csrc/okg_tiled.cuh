@@ -41,6 +41,7 @@ struct TileCfg<2> {
 struct Tiling {
   int32_t ncore;    // core CTAs
   int32_t ktiles, jtiles, ichunk;  // tiles along z, y; planes per CTA along x (= TI)
+  int32_t ci0, ci1;  // interior planes [ci0, ci1) of this slab handled by core CTAs
   uint32_t nbnd;    // boundary vertices
   const uint32_t* __restrict__ bnd;  // boundary vertex indices
 };
@@ -179,8 +180,8 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
   const int ic = DIM == 3 ? b / tl.jtiles : b;
   const int k0 = 1 + kt * TC::TK;
   const int j0 = DIM == 3 ? 1 + jt * TC::TJ : 0;
-  const int i0 = 1 + ic * TI;
-  const int ni = min(TI, g.n - i0);  // planes computed by this CTA
+  const int i0 = tl.ci0 + ic * TI;
+  const int ni = min(TI, tl.ci1 - i0);  // planes computed by this CTA
   const int tk = tid % TC::TK, tj = tid / TC::TK;
   const int k = k0 + tk, j = j0 + tj;
   const bool active = k <= g.n - 1 && (DIM == 2 || j <= g.n - 1);

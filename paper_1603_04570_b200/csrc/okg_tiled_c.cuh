@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled_c(Grid g, Op<DIM> Mo
     const int ic = DIM == 3 ? bb / tl.jtiles : bb;
     const int k0 = 1 + kt * TC::TK;
     const int j0 = DIM == 3 ? 1 + jt * TC::TJ : 0;
-    const int i0 = 1 + ic * TI;
-    const int ni = min(TI, g.n - i0);
+    const int i0 = tl.ci0 + ic * TI;
+    const int ni = min(TI, tl.ci1 - i0);
     const int tk = tid % TC::TK, tj = tid / TC::TK;
     const int k = k0 + tk, j = j0 + tj;
     const bool active = k <= g.n - 1 && (DIM == 2 || j <= g.n - 1);
