@@ -69,6 +69,12 @@ typedef struct okg_params {
                                "up" launch per level): 0 = default (2D: every level
                                but the finest; 3D: levels with n <= 32), 1 = every
                                level, < 0 = never */
+  int32_t nslabs;           /* slab decomposition: split the mesh into this
+                               many x-plane slabs, one host thread + CUDA stream each;
+                               0/1 = one slab.  Results equal the one-slab solve up to
+                               the order of the cross-slab reduction sums. */
+  int32_t slab_devices;     /* 0: every slab on `device` (1-GPU emulation); 1: slab r on
+                               device `device + r` (peer copies over NVLink) */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -106,6 +112,9 @@ typedef struct okg_info {
   int32_t graph_nodes;        /* kernels in the captured Arnoldi graph    */
   int32_t tail_start;         /* first level of the single-CTA tail (-1: none) */
   int32_t tiled_mask;         /* bit l set: level l uses the tiled kernels */
+  int32_t nslabs;             /* slabs of the decomposition (1: none)      */
+  int32_t rep_level;          /* first level replicated on every slab (levels if none) */
+  int32_t slab_ilo[16], slab_ihi[16]; /* owned x-planes [ilo, ihi) of the finest level per slab */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */
@@ -161,7 +170,20 @@ int okg_newton_step(okg_ctx* ctx, okg_step_stats* stats);
 int okg_newton_step_host(okg_ctx* ctx, const double* u_old, const double* w_old,
                          double* u_new, double* w_new, okg_step_stats* stats);
 
-/* ---- per-operator entry points on DEVICE pointers (parity + composition) ---- */
+/* ---- per-operator entry points on HOST pointers (any nslabs) ---------------------
+ * Same operations as the device-pointer entry points below; the context scatters
+ * the inputs over its slabs and gathers the outputs.  With nslabs > 1 okg_apply_host
+ * supports the finest-level kinds (every kind except PROLONG, RESTRICT,
+ * COARSE_SOLVE and SHAT on a level > 0). */
+int okg_linearize_host(okg_ctx* ctx, const double* u);
+int okg_apply_host(okg_ctx* ctx, int32_t kind, int32_t level, const double* x, double* y);
+int okg_residual_host(okg_ctx* ctx, const double* u_next, const double* w_next,
+                      const double* u_old, const double* w_old, double* r1, double* r2);
+int okg_gmres_host(okg_ctx* ctx, const double* b, double* x, double rel_tol, int32_t max_iter,
+                   int32_t restart, okg_krylov_stats* stats);
+
+/* ---- per-operator entry points on DEVICE pointers (parity + composition) ----
+ * single-slab contexts only (OKG_EINVAL when nslabs > 1) */
 /* ctx.Me = assemble_coefficient_mass(mesh, u) (model.hpp:184-185); u on device */
 int okg_linearize(okg_ctx* ctx, const double* u_dev);
 int okg_clear_linearization(okg_ctx* ctx);
@@ -178,7 +200,9 @@ int okg_gmres(okg_ctx* ctx, const double* b_dev, double* x_dev, double rel_tol,
 int okg_jacobi_spectrum(okg_ctx* ctx, double* lo, double* hi);
 
 /* ---- measurement hooks (bench.py) ---------------------------------------- */
-/* the context's CUDA stream (cudaStream_t) -- for events around a region */
+/* the context's CUDA stream (cudaStream_t) -- for events around a region;
+ * with nslabs > 1: slab 0's stream (okg_slab_stream for the others) */
+int okg_slab_stream(okg_ctx* ctx, int32_t slab, void** stream);
 int okg_stream(okg_ctx* ctx, void** stream);
 /* fine-level kernels timed live with CUDA events on the context stream:
  * `which` = OKG_KT_* ; avg_ms = mean launch duration over `reps` launches on

@@ -84,6 +84,8 @@ struct SolverConfig {
   int threads = 1;
   long max_dofs = 2000000;
   int device = 0;
+  int nslabs = 1;          // x-plane slabs; > 1: one host thread + stream each
+  bool slab_devices = false;  // slab r on device `device + r` (else all on `device`)
 
   long num_vertices() const {
     long s = static_cast<long>(n) + 1, v = s * s;
@@ -114,6 +116,8 @@ struct SolverConfig {
     p.max_dofs = max_dofs;
     p.shat_perturb = shat_perturb;
     p.device = device;
+    p.nslabs = nslabs;
+    p.slab_devices = slab_devices ? 1 : 0;
     return p;
   }
   void validate() const {  // SolverConfig::validate
@@ -216,8 +220,8 @@ class SchurContext {
 
   // ctx.Me = assemble_coefficient_mass(mesh, u)   (model.hpp:184-185)
   void set_linearization(const Vector& u) {
-    DeviceVector d(u, device());
-    check(okg_linearize(h_, d.get()));
+    if (static_cast<long>(u.size()) != info_.num_vertices) throw std::invalid_argument("linearization: size mismatch");
+    check(okg_linearize_host(h_, u.data()));
     me_set_ = true;
   }
   void clear_linearization() {
@@ -225,10 +229,11 @@ class SchurContext {
     me_set_ = false;
   }
   Vector apply(int kind, const Vector& x, size_t out_size, int level = 0) const {
-    DeviceVector dx(x, device()), dy(out_size, device());
-    check(okg_apply(h_, kind, level, dx.get(), dy.get()));
-    return dy.host();
+    Vector y(out_size);
+    check(okg_apply_host(h_, kind, level, x.data(), y.data()));
+    return y;
   }
+  int nslabs() const { return info_.nslabs; }
 
  private:
   SolverConfig cfg_;
@@ -285,11 +290,10 @@ inline LinearOperator block_preconditioner(const SchurContext& ctx) {
 inline KrylovResult gmres(const SchurContext& ctx, const Vector& b, double rel_tol, int max_iter, int restart = 0) {
   const int n = ctx.rows();
   if (static_cast<int>(b.size()) != 2 * n) throw std::invalid_argument("gmres: rhs dimension mismatch");
-  DeviceVector db(b, ctx.device()), dx(b.size(), ctx.device());
   okg_krylov_stats ks;
-  check(okg_gmres(ctx.handle(), db.get(), dx.get(), rel_tol, max_iter, restart, &ks));
   KrylovResult r;
-  r.x = dx.host();
+  r.x.resize(b.size());
+  check(okg_gmres_host(ctx.handle(), b.data(), r.x.data(), rel_tol, max_iter, restart, &ks));
   r.iterations = ks.iterations;
   r.converged = ks.converged != 0;
   r.stagnated = ks.stagnated != 0;
@@ -303,10 +307,10 @@ inline std::pair<Vector, Vector> residual(const State& next, const State& old, c
   const size_t n = static_cast<size_t>(ctx.rows());
   if (next.u.size() != old.u.size() || next.w.size() != old.w.size() || next.u.size() != n)
     throw std::invalid_argument("residual: states do not match the mesh");
-  DeviceVector un(next.u, ctx.device()), wn(next.w, ctx.device()), uo(old.u, ctx.device()),
-      wo(old.w, ctx.device()), r1(n, ctx.device()), r2(n, ctx.device());
-  check(okg_residual(ctx.handle(), un.get(), wn.get(), uo.get(), wo.get(), r1.get(), r2.get()));
-  return {r1.host(), r2.host()};
+  Vector r1(n), r2(n);
+  check(okg_residual_host(ctx.handle(), next.u.data(), next.w.data(), old.u.data(), old.w.data(), r1.data(),
+                          r2.data()));
+  return {r1, r2};
 }
 
 inline std::pair<State, IterationStats> newton_solve(const State& old, SchurContext& ctx,

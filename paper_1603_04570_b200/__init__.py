@@ -71,7 +71,7 @@ class SolverConfig:
 
     def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
                   tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
-                  mg_fuse: int = 0) -> _lib.Params:
+                  mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -85,6 +85,8 @@ class SolverConfig:
         p.tail_max_vertices = tail_max_vertices
         p.disable_pdl = 0 if pdl else 1
         p.mg_fuse = mg_fuse
+        p.nslabs = nslabs
+        p.slab_devices = 1 if slab_devices else 0
         return p
 
     def validate(self) -> None:
@@ -233,14 +235,17 @@ class DeviceArray:
 class SchurContext:
     def __init__(self, cfg: SolverConfig, device: int = 0, shat_perturb: float = 0.0,
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
-                 pdl: bool = True, mg_fuse: int = 0):
+                 pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False):
+        """nslabs > 1: x-plane slab decomposition, one host thread + stream per
+        slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
+        `device + r`."""
         if cfg.cheby_precond != "jacobi":
             raise ConfigError("schur context: only cheby_precond = 'jacobi' is implemented on the GPU path")
         self.cfg = cfg
         self.device = device
         self.handle = C.c_void_p()
         check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl,
-                                                    mg_fuse)),
+                                                    mg_fuse, nslabs, slab_devices)),
                              C.byref(self.handle)))
         info = _lib.Info()
         check(lib.okg_get_info(self.handle, C.byref(info)))
@@ -261,6 +266,9 @@ class SchurContext:
         self.graph_nodes = int(info.graph_nodes)
         self.tail_start = int(info.tail_start)
         self.tiled_levels = [l for l in range(self.levels) if (info.tiled_mask >> l) & 1]
+        self.nslabs = int(info.nslabs)
+        self.rep_level = int(info.rep_level)
+        self.slab_planes = [(int(info.slab_ilo[r]), int(info.slab_ihi[r])) for r in range(self.nslabs)]
         self.Me_set = False
 
     def rows(self) -> int:
@@ -293,15 +301,19 @@ class SchurContext:
         check(lib.okg_apply(self.handle, kind, level, x.ptr, y.ptr))
 
     def apply(self, kind: int, x: np.ndarray, level: int = 0) -> np.ndarray:
-        xd = DeviceArray.from_numpy(x, self.device)
-        yd = DeviceArray(self._out_size(kind, level), self.device)
-        self.apply_dev(kind, xd, yd, level)
-        return yd.numpy()
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self._out_size(kind, level))
+        check(lib.okg_apply_host(self.handle, kind, level, x.ctypes.data_as(_lib._dp), y.ctypes.data_as(_lib._dp)))
+        return y
 
     def linearize(self, u: np.ndarray):
         """ctx.Me = assemble_coefficient_mass(mesh, u)  (model.hpp:184-185)."""
-        ud = DeviceArray.from_numpy(u, self.device)
-        check(lib.okg_linearize(self.handle, ud.ptr))
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        check(lib.okg_linearize_host(self.handle, u.ctypes.data_as(_lib._dp)))
+        self.Me_set = True
+
+    def linearize_dev(self, u: DeviceArray):
+        check(lib.okg_linearize(self.handle, u.ptr))
         self.Me_set = True
 
     def clear_linearization(self):
@@ -309,19 +321,21 @@ class SchurContext:
         self.Me_set = False
 
     def residual(self, nxt: State, old: State) -> Tuple[np.ndarray, np.ndarray]:
-        arrs = [DeviceArray.from_numpy(a, self.device) for a in (nxt.u, nxt.w, old.u, old.w)]
-        r1 = DeviceArray(self.n, self.device)
-        r2 = DeviceArray(self.n, self.device)
-        check(lib.okg_residual(self.handle, *[a.ptr for a in arrs], r1.ptr, r2.ptr))
-        return r1.numpy(), r2.numpy()
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (nxt.u, nxt.w, old.u, old.w)]
+        r1 = np.empty(self.n)
+        r2 = np.empty(self.n)
+        check(lib.okg_residual_host(self.handle, *[a.ctypes.data_as(_lib._dp) for a in arrs],
+                                    r1.ctypes.data_as(_lib._dp), r2.ctypes.data_as(_lib._dp)))
+        return r1, r2
 
     def gmres(self, b: np.ndarray, rel_tol: float, max_iter: int, restart: int = 0) -> KrylovResult:
-        bd = DeviceArray.from_numpy(b, self.device)
-        xd = DeviceArray(2 * self.n, self.device)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(2 * self.n)
         ks = _lib.KrylovStats()
-        check(lib.okg_gmres(self.handle, bd.ptr, xd.ptr, rel_tol, max_iter, restart, C.byref(ks)))
+        check(lib.okg_gmres_host(self.handle, b.ctypes.data_as(_lib._dp), x.ctypes.data_as(_lib._dp), rel_tol,
+                                 max_iter, restart, C.byref(ks)))
         nn = min(ks.n_residual_norms, 512)
-        return KrylovResult(xd.numpy(), ks.iterations, list(ks.residual_norms[:nn]), bool(ks.converged),
+        return KrylovResult(x, ks.iterations, list(ks.residual_norms[:nn]), bool(ks.converged),
                             bool(ks.stagnated), ks.final_residual)
 
     def jacobi_spectrum(self) -> Tuple[float, float]:

@@ -44,7 +44,7 @@ class Params(C.Structure):
         ("shat_perturb", C.c_double), ("max_dofs", C.c_int64),
         ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
         ("tail_max_vertices", C.c_int32), ("disable_pdl", C.c_int32),
-        ("mg_fuse", C.c_int32),
+        ("mg_fuse", C.c_int32), ("nslabs", C.c_int32), ("slab_devices", C.c_int32),
     ]
 
 
@@ -72,6 +72,8 @@ class Info(C.Structure):
         ("dt_theta", C.c_double), ("lambda_lo", C.c_double), ("lambda_hi", C.c_double),
         ("eps_sqrt_c", C.c_double), ("device_bytes", C.c_int64), ("graph_nodes", C.c_int32),
         ("tail_start", C.c_int32), ("tiled_mask", C.c_int32),
+        ("nslabs", C.c_int32), ("rep_level", C.c_int32),
+        ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16),
     ]
 
 
@@ -141,6 +143,11 @@ _SIGS = {
     "okg_gmres": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, C.POINTER(KrylovStats)]),
     "okg_jacobi_spectrum": (C.c_int, [_vp, _dp, _dp]),
     "okg_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "okg_slab_stream": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "okg_linearize_host": (C.c_int, [_vp, _dp]),
+    "okg_apply_host": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
+    "okg_residual_host": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "okg_gmres_host": (C.c_int, [_vp, _dp, _dp, C.c_double, C.c_int32, C.c_int32, C.POINTER(KrylovStats)]),
     "okg_kernel_timing": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
     "okg_device_alloc": (C.c_int, [C.c_int32, C.c_size_t, C.POINTER(_vp)]),
     "okg_device_free": (C.c_int, [_vp]),

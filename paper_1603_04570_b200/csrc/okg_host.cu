@@ -154,7 +154,8 @@ struct okg_ctx {
   int L_rep = 1 << 30; // first replicated level
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::vector<std::pair<double*, int>> reg;  // exchange registry: (global-indexed pointer, level)
-  std::vector<okg_ctx*> slabs;               // set only on the handle of a multi-slab context
+  double *io_a = nullptr, *io_b = nullptr, *io_c = nullptr;  // stacked staging of the host-pointer API
+  bool handle = false;  // the user's handle of a multi-slab context (its slabs are group->r)
 };
 
 namespace okg {
@@ -257,6 +258,8 @@ struct Group {
   int done = 0;
   bool stop = false;
   std::vector<int> status;
+  std::vector<std::string> msg;
+  std::atomic<int> first_err{-1};
 
   void barrier() {
     const long g = gen.load(std::memory_order_acquire);
@@ -1551,7 +1554,8 @@ static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double*
       jacobian<DIM>(c, x, y);
       break;
     case OKG_OP_NONLINEAR:
-      launch(c, k_nonlinear<DIM>, nblk(c->N), BS, 0, c->fine, c->nl, x, y);
+      exchange(c, 0, x);
+      launch(c, k_nonlinear<DIM>, own(c->fine), BS, 0, c->fine, c->nl, x, y);
       note(c);
       break;
     case OKG_OP_COARSE_SOLVE: coarse_solve<DIM>(c, x, y); break;
@@ -1628,6 +1632,9 @@ int okg_last_error(char* buf, size_t len) {
   return static_cast<int>(g_err.size());
 }
 
+}  // extern "C"
+
+// ---- contexts ---------------------------------------------------------------------------
 static void destroy_ctx(okg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->p.device);
@@ -1636,60 +1643,278 @@ static void destroy_ctx(okg_ctx* c) {
   if (c->g_prec) cudaGraphExecDestroy(c->g_prec);
   for (void* p : c->allocs) cudaFree(p);
   if (c->hred) cudaFreeHost(c->hred);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 
+// argument checks, derived constants, stream, then build (one slab)
+static void init_ctx(okg_ctx* c) {
+  const okg_params* p = &c->p;
+  // argument checks of build_mesh (mesh.hpp:88-90), make_schur_context (precond.hpp:132-147),
+  // compute_c (precond.hpp:31-38)
+  if (p->dim != 2 && p->dim != 3) THROW(OKG_EINVAL, "build_mesh: dim must be 2 or 3");
+  if (p->n < 1) THROW(OKG_EINVAL, "build_mesh: n must be positive");
+  if (!(p->eps > 0.0)) THROW(OKG_EINVAL, "schur context: eps must be positive");
+  const double scale_factor = 1.0 + p->shat_perturb;
+  if (!(scale_factor > 0.0)) THROW(OKG_EINVAL, "schur context: perturbation must keep the shifted operator positive");
+  if (!(p->dt > 0.0)) THROW(OKG_EINVAL, "compute_c: dt must be positive");
+  if (!(p->theta > 0.0) || p->theta > 1.0) THROW(OKG_EINVAL, "compute_c: theta must lie in (0, 1]");
+  if (p->sigma < 0.0) THROW(OKG_EINVAL, "compute_c: sigma must be nonnegative");
+  if (p->min_coarse_size < 1) THROW(OKG_EINVAL, "build_hierarchy: min_coarse_size < 1");
+  if (p->cheby_iters < 1) THROW(OKG_EINVAL, "chebyshev: need at least one step");
+  if (p->richardson_steps < 1) THROW(OKG_EINVAL, "schur solve: need at least one refinement step");
+  if (p->mg_cycles < 1 || p->mg_pre < 0 || p->mg_post < 0) THROW(OKG_EINVAL, "multigrid: bad cycle settings");
+  if (p->gmres_maxit < 1 || p->gmres_restart < 0) THROW(OKG_EINVAL, "gmres: bad iteration settings");
+  const int64_t s = (int64_t)p->n + 1;
+  const int64_t nv = p->dim == 2 ? s * s : s * s * s;
+  if (nv >= (int64_t)1 << 31) THROW(OKG_EINVAL, "mesh too large for one device (%lld vertices)", (long long)nv);
+  c->dim = p->dim;
+  c->n = p->n;
+  c->c = p->dt * p->theta / (1.0 + p->dt * p->theta * p->sigma);
+  c->sqrt_c = std::sqrt(c->c);
+  c->a_coeff = 1.0 + p->dt * p->theta * p->sigma;
+  c->dt_theta = p->dt * p->theta;
+  c->shat_scale = scale_factor;
+  c->eps_sqrt_c = c->shat_scale * p->eps * c->sqrt_c;
+  CK(cudaSetDevice(p->device));
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  if (c->nslabs > 1) {
+    CK(cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
+  }
+  if (c->dim == 2) build<2>(c);
+  else build<3>(c);
+}
+
+// ---- slab group runtime: one worker thread per slab ---------------------------------------
+static void group_worker(Group* G, int r) {
+  long seen = 0;
+  for (;;) {
+    std::function<void(int)> job;
+    {
+      std::unique_lock<std::mutex> lk(G->jm);
+      G->jcv.wait(lk, [&] { return G->stop || G->jgen != seen; });
+      if (G->stop) return;
+      seen = G->jgen;
+      job = G->job;
+    }
+    job(r);
+    {
+      std::lock_guard<std::mutex> lk(G->jm);
+      if (++G->done == G->S) G->dcv.notify_all();
+    }
+  }
+}
+
+// run f(slab) on every slab thread and wait; every slab's stream is drained before
+// the job counts as done.  Returns the status of the first slab that failed (the
+// others abort at their next barrier).
+static int run_group(Group* G, const std::function<void(int)>& f) {
+  G->count.store(0);
+  G->abort.store(false);
+  G->first_err.store(-1);
+  G->status.assign(G->S, OKG_OK);
+  G->msg.assign(G->S, std::string());
+  {
+    std::lock_guard<std::mutex> lk(G->jm);
+    G->job = [G, &f](int r) {
+      int st = OKG_OK;
+      try {
+        if (G->r[r]) CK(cudaSetDevice(G->r[r]->p.device));
+        f(r);
+        if (G->r[r] && G->r[r]->stream) CK(cudaStreamSynchronize(G->r[r]->stream));
+      } catch (const Status& s) {
+        st = s.code;
+      } catch (const std::bad_alloc&) {
+        st = fail(OKG_ENOMEM, "host allocation failed");
+      } catch (const std::exception& e) {
+        st = fail(OKG_EOTHER, "%s", e.what());
+      }
+      if (st != OKG_OK) {
+        G->status[r] = st;
+        G->msg[r] = g_err;
+        int expect = -1;
+        G->first_err.compare_exchange_strong(expect, r);
+        G->abort.store(true);
+      }
+    };
+    G->done = 0;
+    ++G->jgen;
+  }
+  G->jcv.notify_all();
+  {
+    std::unique_lock<std::mutex> lk(G->jm);
+    G->dcv.wait(lk, [&] { return G->done == G->S; });
+  }
+  const int e = G->first_err.load();
+  if (e < 0) return OKG_OK;
+  g_err = G->msg[e];
+  return G->status[e];
+}
+
+static void destroy_handle(okg_ctx* h) {
+  if (!h) return;
+  if (Group* G = h->group) {
+    if (!G->th.empty()) {
+      run_group(G, [G](int r) {
+        destroy_ctx(G->r[r]);
+        G->r[r] = nullptr;
+      });
+      {
+        std::lock_guard<std::mutex> lk(G->jm);
+        G->stop = true;
+      }
+      G->jcv.notify_all();
+      for (auto& t : G->th) t.join();
+    }
+    delete G;
+  }
+  delete h;
+}
+
+// f(slab context) on every slab of c (on c itself for a one-slab context)
+template <class Fn>
+static int each_slab(okg_ctx* c, Fn&& f) {
+  if (!c->handle)
+    return guard(c, [&] {
+      f(c);
+      CK(cudaStreamSynchronize(c->stream));
+    });
+  Group* G = c->group;
+  return run_group(G, [&](int r) { f(G->r[r]); });
+}
+
+static okg_ctx* slab0(okg_ctx* c) { return c->handle ? c->group->r[0] : c; }
+
+#define SINGLE_SLAB(c, fn)                                                                                    \
+  do {                                                                                                        \
+    if ((c)->handle)                                                                                          \
+      return fail(OKG_EINVAL, "%s: device-pointer entry point on a %d-slab context (use the host-pointer API)", \
+                  fn, (c)->nslabs);                                                                           \
+  } while (0)
+
+// host N-vector blocks <-> the owned planes of a slab's stacked level-0 vector
+static void put_owned(okg_ctx* c, const double* h, double* d, int nb) {
+  const size_t lo = c->fine.lo, cnt = c->fine.hi - c->fine.lo;
+  for (int q = 0; q < nb; ++q)
+    CK(cudaMemcpyAsync(d + (size_t)q * c->B + lo, h + (size_t)q * c->N + lo, cnt * sizeof(double),
+                       cudaMemcpyHostToDevice, c->stream));
+}
+static void get_owned(okg_ctx* c, const double* d, double* h, int nb) {
+  const size_t lo = c->fine.lo, cnt = c->fine.hi - c->fine.lo;
+  for (int q = 0; q < nb; ++q)
+    CK(cudaMemcpyAsync(h + (size_t)q * c->N + lo, d + (size_t)q * c->B + lo, cnt * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream));
+}
+static void ensure_io(okg_ctx* c) {
+  if (c->io_a) return;  // every slab allocates at the same call: registry indices stay aligned
+  c->io_a = lvec(c, c->lv[0], 0, 2);
+  c->io_b = lvec(c, c->lv[0], 0, 2);
+  c->io_c = lvec(c, c->lv[0], 0, 2);
+}
+
+// vector lengths of okg_apply kinds: {input, output} vertex counts
+static void apply_sizes(okg_ctx* c, int kind, int level, size_t& nin, size_t& nout) {
+  const int nlev = static_cast<int>(c->lv.size());
+  nin = nout = c->N;
+  switch (kind) {
+    case OKG_OP_BLOCK: case OKG_OP_JACOBIAN: nin = nout = 2 * (size_t)c->N; break;
+    case OKG_OP_SHAT:
+      if (level < 0 || level >= nlev) THROW(OKG_EINVAL, "level out of range");
+      nin = nout = c->lv[level].g.N;
+      break;
+    case OKG_OP_PROLONG:
+      if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
+      nin = c->lv[level + 1].g.N;
+      nout = c->lv[level].g.N;
+      break;
+    case OKG_OP_RESTRICT:
+      if (level < 0 || level + 1 >= nlev) THROW(OKG_EINVAL, "level out of range");
+      nin = c->lv[level].g.N;
+      nout = c->lv[level + 1].g.N;
+      break;
+    case OKG_OP_COARSE_SOLVE: nin = nout = c->lv.back().g.N; break;
+    default: break;
+  }
+}
+
+extern "C" {
+
 int okg_create(const okg_params* p, okg_ctx** out) {
   if (!p || !out) return fail(OKG_EINVAL, "okg_create: null argument");
   *out = nullptr;
-  okg_ctx* c = new okg_ctx();
-  c->p = *p;
-  const int st = guard(nullptr, [&] {
-    // argument checks of build_mesh (mesh.hpp:88-90), make_schur_context (precond.hpp:132-147),
-    // compute_c (precond.hpp:31-38)
-    if (p->dim != 2 && p->dim != 3) THROW(OKG_EINVAL, "build_mesh: dim must be 2 or 3");
-    if (p->n < 1) THROW(OKG_EINVAL, "build_mesh: n must be positive");
-    if (!(p->eps > 0.0)) THROW(OKG_EINVAL, "schur context: eps must be positive");
-    const double scale_factor = 1.0 + p->shat_perturb;
-    if (!(scale_factor > 0.0))
-      THROW(OKG_EINVAL, "schur context: perturbation must keep the shifted operator positive");
-    if (!(p->dt > 0.0)) THROW(OKG_EINVAL, "compute_c: dt must be positive");
-    if (!(p->theta > 0.0) || p->theta > 1.0) THROW(OKG_EINVAL, "compute_c: theta must lie in (0, 1]");
-    if (p->sigma < 0.0) THROW(OKG_EINVAL, "compute_c: sigma must be nonnegative");
-    if (p->min_coarse_size < 1) THROW(OKG_EINVAL, "build_hierarchy: min_coarse_size < 1");
-    if (p->cheby_iters < 1) THROW(OKG_EINVAL, "chebyshev: need at least one step");
-    if (p->richardson_steps < 1) THROW(OKG_EINVAL, "schur solve: need at least one refinement step");
-    if (p->mg_cycles < 1 || p->mg_pre < 0 || p->mg_post < 0) THROW(OKG_EINVAL, "multigrid: bad cycle settings");
-    if (p->gmres_maxit < 1 || p->gmres_restart < 0) THROW(OKG_EINVAL, "gmres: bad iteration settings");
-    const int64_t s = (int64_t)p->n + 1;
-    const int64_t nv = p->dim == 2 ? s * s : s * s * s;
-    if (nv >= (int64_t)1 << 31) THROW(OKG_EINVAL, "mesh too large for one device (%lld vertices)", (long long)nv);
-    c->dim = p->dim;
-    c->n = p->n;
-    c->c = p->dt * p->theta / (1.0 + p->dt * p->theta * p->sigma);
-    c->sqrt_c = std::sqrt(c->c);
-    c->a_coeff = 1.0 + p->dt * p->theta * p->sigma;
-    c->dt_theta = p->dt * p->theta;
-    c->shat_scale = scale_factor;
-    c->eps_sqrt_c = c->shat_scale * p->eps * c->sqrt_c;
-    CK(cudaSetDevice(p->device));
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    if (c->dim == 2) build<2>(c);
-    else build<3>(c);
+  const int S = p->nslabs < 1 ? 1 : p->nslabs;
+  if (S > 16) return fail(OKG_EINVAL, "okg_create: at most 16 slabs (nslabs = %d)", S);
+  if (S == 1) {
+    okg_ctx* c = new okg_ctx();
+    c->p = *p;
+    c->p.nslabs = 1;
+    const int st = guard(nullptr, [&] { init_ctx(c); });
+    if (st != OKG_OK) {
+      destroy_ctx(c);
+      return st;
+    }
+    *out = c;
+    return OKG_OK;
+  }
+  // several slabs: a handle + one worker thread (own stream, own device buffers) per slab
+  okg_ctx* h = new okg_ctx();
+  h->p = *p;
+  h->handle = true;
+  h->nslabs = S;
+  h->dim = p->dim;
+  h->n = p->n;
+  Group* G = new Group();
+  G->S = S;
+  G->r.assign(S, nullptr);
+  G->scratch.assign((size_t)S * 256, 0.0);
+  h->group = G;
+  for (int r = 0; r < S; ++r) G->th.emplace_back(group_worker, G, r);
+  const int st = run_group(G, [&](int r) {
+    okg_ctx* c = new okg_ctx();
+    c->p = *p;
+    c->p.device = p->device + (p->slab_devices ? r : 0);
+    c->p.use_graphs = 0;  // cross-slab exchanges are host-ordered: not capturable
+    c->rank = r;
+    c->nslabs = S;
+    c->group = G;
+    G->r[r] = c;  // published before the first barrier of build()
+    CK(cudaSetDevice(c->p.device));
+    if (p->slab_devices)
+      for (int q = 0; q < S; ++q) {
+        const int dq = p->device + q;
+        int ok = 0;
+        if (dq == c->p.device || cudaDeviceCanAccessPeer(&ok, c->p.device, dq) != cudaSuccess || !ok) continue;
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dq, 0);
+        if (e != cudaSuccess) (void)cudaGetLastError();  // already enabled / staged copies still work
+      }
+    init_ctx(c);
   });
   if (st != OKG_OK) {
-    destroy_ctx(c);
+    destroy_handle(h);
     return st;
   }
-  *out = c;
+  okg_ctx* c0 = G->r[0];
+  h->N = c0->N;
+  h->c = c0->c;
+  h->sqrt_c = c0->sqrt_c;
+  h->a_coeff = c0->a_coeff;
+  h->dt_theta = c0->dt_theta;
+  h->eps_sqrt_c = c0->eps_sqrt_c;
+  *out = h;
   return OKG_OK;
 }
 
-void okg_destroy(okg_ctx* c) { destroy_ctx(c); }
+void okg_destroy(okg_ctx* c) {
+  if (c && c->handle) destroy_handle(c);
+  else destroy_ctx(c);
+}
 
-int okg_get_info(okg_ctx* c, okg_info* info) {
-  if (!c || !info) return fail(OKG_EINVAL, "null argument");
+int okg_get_info(okg_ctx* h, okg_info* info) {
+  if (!h || !info) return fail(OKG_EINVAL, "null argument");
+  okg_ctx* c = slab0(h);
   std::memset(info, 0, sizeof *info);
   info->dim = c->dim;
   info->n = c->n;
@@ -1706,11 +1931,18 @@ int okg_get_info(okg_ctx* c, okg_info* info) {
   info->lambda_lo = c->lambda_lo;
   info->lambda_hi = c->lambda_hi;
   info->eps_sqrt_c = c->eps_sqrt_c;
-  info->device_bytes = static_cast<int64_t>(c->bytes);
   info->graph_nodes = c->arn_nodes;
   info->tail_start = c->tail_start;
   for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
     if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
+  info->nslabs = h->handle ? h->nslabs : 1;
+  info->rep_level = std::min<int>(c->L_rep, (int)c->lv.size());
+  for (int r = 0; r < info->nslabs; ++r) {
+    okg_ctx* s = h->handle ? h->group->r[r] : h;
+    info->device_bytes += static_cast<int64_t>(s->bytes);
+    info->slab_ilo[r] = s->fine.ilo;
+    info->slab_ihi[r] = s->fine.ihi;
+  }
   return OKG_OK;
 }
 
@@ -1777,62 +2009,160 @@ int okg_seeded_ic(int64_t nverts, uint64_t seed, double m, double* u) {
 
 int okg_set_state(okg_ctx* c, const double* u, const double* w, double t, int32_t step) {
   if (!c || !u || !w) return fail(OKG_EINVAL, "okg_set_state: null argument");
-  return guard(c, [&] {
-    CK(cudaMemcpyAsync(c->u_old, u, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->w_old, w, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    c->t = t;
-    c->step = step;
+  return each_slab(c, [&](okg_ctx* s) {
+    put_owned(s, u, s->u_old, 1);
+    put_owned(s, w, s->w_old, 1);
+    s->t = t;
+    s->step = step;
   });
 }
 
 int okg_get_state(okg_ctx* c, double* u, double* w, double* t, int32_t* step) {
   if (!c) return fail(OKG_EINVAL, "okg_get_state: null context");
-  return guard(c, [&] {
-    if (u) CK(cudaMemcpyAsync(u, c->u_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (w) CK(cudaMemcpyAsync(w, c->w_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    if (t) *t = c->t;
-    if (step) *step = c->step;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    if (u) get_owned(s, s->u_old, u, 1);
+    if (w) get_owned(s, s->w_old, w, 1);
   });
+  if (st == OKG_OK) {
+    if (t) *t = slab0(c)->t;
+    if (step) *step = slab0(c)->step;
+  }
+  return st;
+}
+
+// newton_solve on every slab; the statistics are slab 0's (every slab takes the same
+// decisions: all scalars are allreduced), launches and seconds cover the whole group
+static int newton_all(okg_ctx* c, const double* u_old, const double* w_old, double* u_new, double* w_new,
+                      okg_step_stats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const long long l0 = g_launches.load();
+  okg_step_stats s0;
+  std::memset(&s0, 0, sizeof s0);
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    okg_step_stats ss;
+    if (u_old) put_owned(s, u_old, s->u_old, 1);
+    if (w_old) put_owned(s, w_old, s->w_old, 1);
+    DISPATCH(s, newton_step_impl, s, &ss);
+    if (u_new) get_owned(s, s->u_old, u_new, 1);
+    if (w_new) get_owned(s, s->w_old, w_new, 1);
+    if (s->rank == 0) s0 = ss;
+  });
+  if (st == OKG_OK && stats) {
+    *stats = s0;
+    stats->kernel_launches = g_launches.load() - l0;
+    stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return st;
 }
 
 int okg_newton_step(okg_ctx* c, okg_step_stats* stats) {
   if (!c) return fail(OKG_EINVAL, "okg_newton_step: null context");
-  return guard(c, [&] { DISPATCH(c, newton_step_impl, c, stats); });
+  return newton_all(c, nullptr, nullptr, nullptr, nullptr, stats);
 }
 
 int okg_newton_step_host(okg_ctx* c, const double* u_old, const double* w_old, double* u_new, double* w_new,
                          okg_step_stats* stats) {
   if (!c || !u_old || !w_old || !u_new || !w_new) return fail(OKG_EINVAL, "okg_newton_step_host: null argument");
-  return guard(c, [&] {
-    const auto t0 = std::chrono::steady_clock::now();
-    CK(cudaMemcpyAsync(c->u_old, u_old, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->w_old, w_old, c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    DISPATCH(c, newton_step_impl, c, stats);
-    CK(cudaMemcpyAsync(u_new, c->u_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(w_new, c->w_old, c->N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    if (stats) stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return newton_all(c, u_old, w_old, u_new, w_new, stats);
+}
+
+int okg_clear_linearization(okg_ctx* c) {
+  if (!c) return fail(OKG_EINVAL, "null context");
+  if (c->handle)
+    for (okg_ctx* s : c->group->r) s->have_lin = false;
+  else
+    c->have_lin = false;
+  return OKG_OK;
+}
+
+// ---- host-pointer entry points (any number of slabs) -------------------------------------
+int okg_linearize_host(okg_ctx* c, const double* u) {
+  if (!c || !u) return fail(OKG_EINVAL, "okg_linearize_host: null argument");
+  return each_slab(c, [&](okg_ctx* s) {
+    ensure_io(s);
+    put_owned(s, u, s->io_a, 1);
+    DISPATCH(s, linearize, s, s->io_a);
   });
 }
 
+int okg_apply_host(okg_ctx* c, int32_t kind, int32_t level, const double* x, double* y) {
+  if (!c || !x || !y) return fail(OKG_EINVAL, "okg_apply_host: null argument");
+  if (kind < OKG_OP_M || kind > OKG_OP_COARSE_SOLVE) return fail(OKG_EINVAL, "okg_apply_host: unknown kind %d", kind);
+  const bool level0 = !(kind == OKG_OP_PROLONG || kind == OKG_OP_RESTRICT || kind == OKG_OP_COARSE_SOLVE ||
+                        (kind == OKG_OP_SHAT && level != 0));
+  if (c->handle && !level0)
+    return fail(OKG_EINVAL, "okg_apply_host: kind %d on level %d needs a one-slab context", kind, level);
+  return each_slab(c, [&](okg_ctx* s) {
+    if (level0) {
+      const int nb = (kind == OKG_OP_BLOCK || kind == OKG_OP_JACOBIAN) ? 2 : 1;
+      ensure_io(s);
+      put_owned(s, x, s->io_a, nb);
+      DISPATCH(s, apply_impl, s, kind, level, s->io_a, s->io_b);
+      get_owned(s, s->io_b, y, nb);
+    } else {
+      size_t nin = 0, nout = 0;
+      apply_sizes(s, kind, level, nin, nout);
+      double* dx = dalloc(s, nin);
+      double* dy = dalloc(s, nout);
+      CK(cudaMemcpyAsync(dx, x, nin * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+      DISPATCH(s, apply_impl, s, kind, level, dx, dy);
+      CK(cudaMemcpyAsync(y, dy, nout * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      CK(cudaStreamSynchronize(s->stream));
+      for (double* q : {dx, dy}) {
+        cudaFree(q);
+        s->allocs.erase(std::find(s->allocs.begin(), s->allocs.end(), (void*)q));
+      }
+      s->bytes -= (nin + nout) * sizeof(double);
+    }
+  });
+}
+
+int okg_residual_host(okg_ctx* c, const double* un, const double* wn, const double* uo, const double* wo, double* r1,
+                      double* r2) {
+  if (!c || !un || !wn || !uo || !wo || !r1 || !r2) return fail(OKG_EINVAL, "okg_residual_host: null argument");
+  return each_slab(c, [&](okg_ctx* s) {
+    ensure_io(s);
+    put_owned(s, un, s->io_a, 1);
+    put_owned(s, wn, s->io_a + s->B, 1);
+    put_owned(s, uo, s->io_b, 1);
+    put_owned(s, wo, s->io_b + s->B, 1);
+    DISPATCH(s, residual, s, s->io_a, s->io_a + s->B, s->io_b, s->io_b + s->B, s->io_c, s->io_c + s->B, 1.0,
+             nullptr);
+    get_owned(s, s->io_c, r1, 1);
+    get_owned(s, s->io_c + s->B, r2, 1);
+  });
+}
+
+int okg_gmres_host(okg_ctx* c, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t restart,
+                   okg_krylov_stats* stats) {
+  if (!c || !b || !x) return fail(OKG_EINVAL, "okg_gmres_host: null argument");
+  okg_krylov_stats k0;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    check_lin(s, "jacobian apply");
+    ensure_io(s);
+    put_owned(s, b, s->io_a, 2);
+    okg_krylov_stats ks;
+    DISPATCH(s, gmres, s, s->io_a, s->io_b, rel_tol, max_iter, restart, &ks, -1.0);
+    get_owned(s, s->io_b, x, 2);
+    if (s->rank == 0) k0 = ks;
+  });
+  if (st == OKG_OK && stats) *stats = k0;
+  return st;
+}
+
+// ---- device-pointer entry points (one slab) ------------------------------------------------
 int okg_linearize(okg_ctx* c, const double* u_dev) {
   if (!c || !u_dev) return fail(OKG_EINVAL, "okg_linearize: null argument");
+  SINGLE_SLAB(c, "okg_linearize");
   return guard(c, [&] {
     DISPATCH(c, linearize, c, u_dev);
     CK(cudaStreamSynchronize(c->stream));
   });
 }
 
-int okg_clear_linearization(okg_ctx* c) {
-  if (!c) return fail(OKG_EINVAL, "null context");
-  c->have_lin = false;
-  return OKG_OK;
-}
-
 int okg_apply(okg_ctx* c, int32_t kind, int32_t level, const double* x, double* y) {
   if (!c || !x || !y) return fail(OKG_EINVAL, "okg_apply: null argument");
+  SINGLE_SLAB(c, "okg_apply");
   return guard(c, [&] {
     DISPATCH(c, apply_impl, c, kind, level, x, y);
     CK(cudaStreamSynchronize(c->stream));
@@ -1842,12 +2172,14 @@ int okg_apply(okg_ctx* c, int32_t kind, int32_t level, const double* x, double* 
 int okg_residual(okg_ctx* c, const double* un, const double* wn, const double* uo, const double* wo, double* r1,
                  double* r2) {
   if (!c || !un || !wn || !uo || !wo || !r1 || !r2) return fail(OKG_EINVAL, "okg_residual: null argument");
+  SINGLE_SLAB(c, "okg_residual");
   return guard(c, [&] { DISPATCH(c, residual, c, un, wn, uo, wo, r1, r2, 1.0, nullptr); });
 }
 
 int okg_gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int32_t max_iter, int32_t restart,
               okg_krylov_stats* stats) {
   if (!c || !b || !x) return fail(OKG_EINVAL, "okg_gmres: null argument");
+  SINGLE_SLAB(c, "okg_gmres");
   return guard(c, [&] {
     check_lin(c, "jacobian apply");
     DISPATCH(c, gmres, c, b, x, rel_tol, max_iter, restart, stats, -1.0);
@@ -1857,12 +2189,33 @@ int okg_gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int32_t ma
 
 int okg_jacobi_spectrum(okg_ctx* c, double* lo, double* hi) {
   if (!c || !lo || !hi) return fail(OKG_EINVAL, "null argument");
-  return guard(c, [&] { DISPATCH(c, jacobi_spectrum, c, *lo, *hi); });
+  double l0 = 0, h0 = 0;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    double a = 0, b = 0;
+    DISPATCH(s, jacobi_spectrum, s, a, b);
+    if (s->rank == 0) {
+      l0 = a;
+      h0 = b;
+    }
+  });
+  if (st == OKG_OK) {
+    *lo = l0;
+    *hi = h0;
+  }
+  return st;
 }
 
 int okg_stream(okg_ctx* c, void** stream) {
   if (!c || !stream) return fail(OKG_EINVAL, "null argument");
-  *stream = reinterpret_cast<void*>(c->stream);
+  *stream = reinterpret_cast<void*>(slab0(c)->stream);
+  return OKG_OK;
+}
+
+int okg_slab_stream(okg_ctx* c, int32_t slab, void** stream) {
+  if (!c || !stream) return fail(OKG_EINVAL, "null argument");
+  const int S = c->handle ? c->nslabs : 1;
+  if (slab < 0 || slab >= S) return fail(OKG_EINVAL, "okg_slab_stream: slab %d out of range", slab);
+  *stream = reinterpret_cast<void*>((c->handle ? c->group->r[slab] : c)->stream);
   return OKG_OK;
 }
 
@@ -1966,6 +2319,7 @@ extern "C" {
 
 int okg_kernel_timing(okg_ctx* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {
   if (!c || !avg_ms || !bytes || reps < 1) return fail(OKG_EINVAL, "okg_kernel_timing: bad argument");
+  SINGLE_SLAB(c, "okg_kernel_timing");
   return guard(c, [&] { DISPATCH(c, kernel_timing_impl, c, which, reps, avg_ms, bytes); });
 }
 
