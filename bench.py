@@ -44,6 +44,15 @@ WORKLOADS = {
                 "BASELINE configs[0]: 2D 64^2, seed 0"),
 }
 
+# N > 1 (torchrun, one process per GPU, one x-plane slab each): weak scaling keeps
+# the vertices per GPU about fixed with meshes whose hierarchy still coarsens to a
+# small direct-solve grid (n = 2^k * odd, coarsest <= 2000 vertices)
+WEAK_N = {
+    "c4_3d128": {1: 128, 2: 160, 4: 192, 8: 256},      # 2.15M, 2.09M, 1.80M, 2.12M vertices per GPU
+    "c2_2d2048": {1: 2048, 2: 2944, 4: 4096, 8: 5888},  # 4.20M, 4.34M, 4.20M, 4.33M vertices per GPU
+    "c1_2d64": {1: 64, 2: 96, 4: 128, 8: 192},
+}
+
 # dominant kernel for the roofline object (top kernel by share of the step in
 # the committed ncu launch list, profiles/)
 DOMINANT = "smooth"
@@ -177,6 +186,8 @@ def main():
     ap.add_argument("--workload", default="c4_3d128", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of reference CPU work (cpu_baseline)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = mesh grows with N (WEAK_N), strong = the workload's mesh split N ways")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -200,10 +211,22 @@ def main():
     import ctypes as C
 
     dim, n, eps, m, seed, n_cpu, desc = WORKLOADS[args.workload]
+    if world > 1 and args.scaling == "weak":
+        n = WEAK_N[args.workload].get(world)
+        if n is None:
+            raise SystemExit(f"--scaling weak: no mesh for {world} GPUs (have {sorted(WEAK_N[args.workload])})")
     cfg = okg.SolverConfig(dim=dim, n=n, eps=eps, m=m, sigma=100.0, theta=0.5, dt=eps * eps,
                            newton_tol=1e-8, gmres_tol=1e-10, gmres_restart=30)
     t0 = time.time()
-    ctx = okg.SchurContext(cfg, device=device)
+    if world > 1:
+        # one slab per process: rank 0 makes the NCCL id of the solver's own communicator
+        idt = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{device}")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(okg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        ctx = okg.SchurContext(cfg, device=device, rank=rank, nranks=world, nccl_id=bytes(idt.cpu().numpy()))
+    else:
+        ctx = okg.SchurContext(cfg, device=device)
     setup_s = time.time() - t0
     N = ctx.n
     u0 = okg.seeded_ic(N, seed, m)
@@ -245,7 +268,7 @@ def main():
     if dist is not None:
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
     t_max_ms = float(t_tensor.item())
-    value = world * dofs / (t_max_ms * 1e-3)
+    value = dofs / (t_max_ms * 1e-3)  # dofs counts the whole mesh (all slabs) once
 
     # ---- e2e: through the C ABI with pinned host buffers, H2D/D2H inside ----
     hu_in = torch.from_numpy(u0.copy()).pin_memory()
@@ -271,7 +294,11 @@ def main():
     e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{device}")
     if dist is not None:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * e2e_dofs / (float(e2e_t.item()) * 1e-3)
+    e2e_value = e2e_dofs / (float(e2e_t.item()) * 1e-3)
+    lt = torch.tensor([launches], dtype=torch.int64, device=f"cuda:{device}")
+    if dist is not None:
+        dist.all_reduce(lt)  # kernels of every rank
+    launches = int(lt.item())
 
     # ---- per-kernel live timing (CUDA events on the solver stream) ----
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -322,10 +349,12 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded IC u0 = m + 0.01 U(-1,1), SURVEY.md 8(d); no dataset involved)",
             "config": {"workload": args.workload, "description": desc, "dim": dim, "n": n, "dofs": 2 * N,
-                       "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas (slab split not yet)",
+                       "parallelism": "1 GPU" if world == 1 else
+                       (f"{world} x-plane slabs, one per GPU/process; ghost planes by NCCL send/recv, "
+                        f"Krylov sums by NCCL allreduce; planes per rank {ctx.slab_planes}"),
                        "l2": "per-step working set (1.1 GB Krylov basis) >> 126 MB L2; no flush",
                        "setup_s": setup_s, "levels": ctx.level_sizes},
             "newton_iters": [s.newton_iters for s in stats],

@@ -153,6 +153,25 @@ int okg_create(const okg_params* p, okg_ctx** ctx);
 void okg_destroy(okg_ctx* ctx);
 int okg_get_info(okg_ctx* ctx, okg_info* info);
 
+/* ---- one process per GPU ------------------------------------------
+ * Rank `rank` of `nranks` processes, each owning the x-plane slab of the mesh the
+ * partition below assigns it, on its own GPU `p->device`.  Ghost planes travel by
+ * NCCL send/recv between neighbours and the Krylov/Lanczos sums by NCCL allreduce
+ * (libnccl.so.2 is loaded at run time).  Rank 0 makes the id with
+ * okg_nccl_unique_id; the caller hands it to every rank (e.g. a
+ * torch.distributed broadcast).  Host-pointer entry points take full-size arrays
+ * and read/write the rank's own planes only; device-pointer ones are refused.
+ * nranks = 1 with a null id is an ordinary one-slab context. */
+int okg_nccl_unique_id(void* id, size_t len); /* len >= 128 */
+int okg_create_rank(const okg_params* p, int32_t rank, int32_t nranks, const void* nccl_id,
+                    okg_ctx** ctx);
+/* the slab partition (pure host; the same function the contexts use): levels of the
+ * hierarchy, first level replicated on every slab, and the owned planes [lo[l], hi[l])
+ * of `rank` on every level (all planes on replicated levels); lo/hi hold 32 entries */
+int okg_slab_partition(int32_t dim, int32_t n, int32_t min_coarse_size, int32_t nslabs,
+                       int32_t rank, int32_t* levels, int32_t* rep_level, int32_t* lo,
+                       int32_t* hi);
+
 /* build_mesh arrays, bit-exact (mesh.hpp:87-157); host memory.
  * vertices: N*dim doubles; cells: (2n^2 | 6n^3)*(dim+1) int32 */
 int okg_mesh(int32_t dim, int32_t n, double* vertices, int32_t* cells);

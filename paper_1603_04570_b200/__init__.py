@@ -155,6 +155,23 @@ def build_mesh(dim: int, n: int, with_arrays: bool = True) -> StructuredMesh:
     return StructuredMesh(dim, n, 1.0 / n, v, c)
 
 
+def nccl_unique_id() -> bytes:
+    """The 128-byte NCCL id rank 0 makes for okg_create_rank (share it with every rank)."""
+    buf = C.create_string_buffer(128)
+    check(lib.okg_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def slab_partition(dim: int, n: int, nslabs: int, rank: int, min_coarse_size: int = 500):
+    """The slab partition the contexts use (okg_slab_partition): returns
+    (levels, rep_level, [(lo, hi) owned x-planes per level])."""
+    lv, rep = C.c_int32(), C.c_int32()
+    lo = (C.c_int32 * 32)()
+    hi = (C.c_int32 * 32)()
+    check(lib.okg_slab_partition(dim, n, min_coarse_size, nslabs, rank, C.byref(lv), C.byref(rep), lo, hi))
+    return lv.value, rep.value, [(lo[l], hi[l]) for l in range(lv.value)]
+
+
 def seeded_ic(nverts: int, seed: int, m: float) -> np.ndarray:
     """Builder-defined seeded IC of SURVEY.md 8(d): u0 = m + 0.01*U(-1,1), splitmix64(seed, vertex)."""
     u = np.empty(nverts)
@@ -235,18 +252,26 @@ class DeviceArray:
 class SchurContext:
     def __init__(self, cfg: SolverConfig, device: int = 0, shat_perturb: float = 0.0,
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
-                 pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False):
+                 pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
+                 rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None):
         """nslabs > 1: x-plane slab decomposition, one host thread + stream per
         slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
-        `device + r`."""
+        `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
+        process owning slab `rank`; host arrays stay full-size, the rank reads/writes its
+        own planes."""
         if cfg.cheby_precond != "jacobi":
             raise ConfigError("schur context: only cheby_precond = 'jacobi' is implemented on the GPU path")
         self.cfg = cfg
         self.device = device
         self.handle = C.c_void_p()
-        check(lib.okg_create(C.byref(cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl,
-                                                    mg_fuse, nslabs, slab_devices)),
-                             C.byref(self.handle)))
+        params = cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl, mg_fuse,
+                               nslabs, slab_devices)
+        if rank is None:
+            check(lib.okg_create(C.byref(params), C.byref(self.handle)))
+        else:
+            idbuf = C.create_string_buffer(bytes(nccl_id), len(nccl_id)) if nccl_id is not None else None
+            check(lib.okg_create_rank(C.byref(params), rank, nranks, idbuf, C.byref(self.handle)))
+        self.rank = 0 if rank is None else rank
         info = _lib.Info()
         check(lib.okg_get_info(self.handle, C.byref(info)))
         self.info = info

@@ -144,6 +144,11 @@ _SIGS = {
     "okg_jacobi_spectrum": (C.c_int, [_vp, _dp, _dp]),
     "okg_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "okg_slab_stream": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
+    "okg_nccl_unique_id": (C.c_int, [_vp, C.c_size_t]),
+    "okg_create_rank": (C.c_int, [C.POINTER(Params), C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
+    "okg_slab_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32)]),
     "okg_linearize_host": (C.c_int, [_vp, _dp]),
     "okg_apply_host": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
     "okg_residual_host": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp]),

@@ -28,10 +28,12 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/okg.h"
 #include "okg_kernels.cuh"
+#include "okg_nccl.h"
 #include "okg_tables.h"
 
 namespace okg {
@@ -62,6 +64,13 @@ static int fail(int code, const char* fmt, ...) {
   } while (0)
 
 #define THROW(code, ...) throw Status{fail(code, __VA_ARGS__)}
+
+#define NCK(c, call)                                                                   \
+  do {                                                                                 \
+    ncclResult_t r__ = (call);                                                         \
+    if (r__ != ncclSuccess)                                                            \
+      throw Status{fail(OKG_ECUDA, "%s: %s", #call, (c)->ncl->GetErrorString(r__))};    \
+  } while (0)
 
 struct HostOp {
   double w[15];
@@ -156,6 +165,10 @@ struct okg_ctx {
   std::vector<std::pair<double*, int>> reg;  // exchange registry: (global-indexed pointer, level)
   double *io_a = nullptr, *io_b = nullptr, *io_c = nullptr;  // stacked staging of the host-pointer API
   bool handle = false;  // the user's handle of a multi-slab context (its slabs are group->r)
+  // one process per GPU (okg_create_rank): the slab transport is NCCL instead of the group
+  ncclComm_t comm = nullptr;
+  const NcclApi* ncl = nullptr;
+  std::vector<int> rep_lo, rep_hi;  // per slab: planes of the first replicated level it restricts into
 };
 
 namespace okg {
@@ -276,9 +289,18 @@ struct Group {
   }
 };
 
+static void write_red(okg_ctx* c, int off, int cnt);
+static void sync_read(okg_ctx* c, int off, int cnt);
+
 static void allreduce(okg_ctx* c, int off, int cnt) {
+  if (c->nslabs == 1) return;
+  if (c->comm) {  // one process per GPU: NCCL allreduce of the staged sums (same result on every rank)
+    write_red(c, off, cnt);
+    NCK(c, c->ncl->AllReduce(c->dred + off, c->dred + off, cnt, ncclDouble, ncclSum, c->comm, c->stream));
+    sync_read(c, off, cnt);
+    return;
+  }
   Group* G = c->group;
-  if (!G || G->S == 1) return;
   for (int i = 0; i < cnt; ++i) G->scratch[(size_t)c->rank * 256 + i] = c->hred[off + i];
   G->barrier();
   for (int i = 0; i < cnt; ++i) {
@@ -302,10 +324,25 @@ static int reg_index(okg_ctx* c, const double* x, int l) {
 
 // refresh the ghost planes of level-l vector x from the neighbouring slabs
 static void exchange(okg_ctx* c, int l, const double* x) {
-  Group* G = c->group;
-  if (!G || G->S == 1) return;
+  if (c->nslabs == 1) return;
   const Level& L = c->lv[l];
   if (L.gh == 0) return;
+  if (c->comm) {  // NCCL: boundary planes out, ghost planes in, both neighbours in one group
+    double* v = const_cast<double*>(x);
+    const size_t ps = L.g.ps;
+    NCK(c, c->ncl->GroupStart());
+    if (c->rank > 0) {
+      NCK(c, c->ncl->Send(v + (size_t)L.g.ilo * ps, ps, ncclDouble, c->rank - 1, c->comm, c->stream));
+      NCK(c, c->ncl->Recv(v + (size_t)(L.g.ilo - 1) * ps, ps, ncclDouble, c->rank - 1, c->comm, c->stream));
+    }
+    if (c->rank + 1 < c->nslabs) {
+      NCK(c, c->ncl->Send(v + (size_t)(L.g.ihi - 1) * ps, ps, ncclDouble, c->rank + 1, c->comm, c->stream));
+      NCK(c, c->ncl->Recv(v + (size_t)L.g.ihi * ps, ps, ncclDouble, c->rank + 1, c->comm, c->stream));
+    }
+    NCK(c, c->ncl->GroupEnd());
+    return;
+  }
+  Group* G = c->group;
   const int q = reg_index(c, x, l);
   const size_t pb = (size_t)L.g.ps * sizeof(double);
   CK(cudaEventRecord(c->ev_a, c->stream));
@@ -328,10 +365,24 @@ static void exchange(okg_ctx* c, int l, const double* x) {
 // replicated level l: every slab computed the planes of its restriction range;
 // copy them to all other slabs
 static void allgather_planes(okg_ctx* c, int l, double* x) {
-  Group* G = c->group;
-  if (!G || G->S == 1) return;
-  const int q = reg_index(c, x, l);
+  if (c->nslabs == 1) return;
   const Level& L = c->lv[l];
+  if (c->comm) {
+    const size_t ps = L.g.ps;
+    const int a = c->rep_lo[c->rank], b = c->rep_hi[c->rank];
+    NCK(c, c->ncl->GroupStart());
+    for (int o = 0; o < c->nslabs; ++o) {
+      if (o == c->rank) continue;
+      if (b > a) NCK(c, c->ncl->Send(x + (size_t)a * ps, (size_t)(b - a) * ps, ncclDouble, o, c->comm, c->stream));
+      if (c->rep_hi[o] > c->rep_lo[o])
+        NCK(c, c->ncl->Recv(x + (size_t)c->rep_lo[o] * ps, (size_t)(c->rep_hi[o] - c->rep_lo[o]) * ps, ncclDouble, o,
+                           c->comm, c->stream));
+    }
+    NCK(c, c->ncl->GroupEnd());
+    return;
+  }
+  Group* G = c->group;
+  const int q = reg_index(c, x, l);
   CK(cudaEventRecord(c->ev_a, c->stream));
   G->barrier();
   for (int o = 0; o < G->S; ++o) {
@@ -348,6 +399,39 @@ static void allgather_planes(okg_ctx* c, int l, double* x) {
   G->barrier();
   for (int o = 0; o < G->S; ++o)
     if (o != c->rank) CK(cudaStreamWaitEvent(c->stream, G->r[o]->ev_b, 0));
+}
+
+// Slab partition: whole x-planes; boundaries even on the finest
+// level, so that coarse ranges nest ((a+1)/2: coarse plane G is owned iff fine
+// plane 2G is); from the first level where some slab would keep < 2 planes on
+// (and always the coarsest), levels are replicated on every slab.  Writes the
+// owned planes [lo[l], hi[l]) of `rank` for every split level and returns the
+// first replicated level.  s0 = planes of the finest level, nlev = levels.
+static int slab_partition(int s0, int nlev, int S, int rank, int* lo, int* hi) {
+  auto fine = [&](int r, int& a, int& b) {
+    a = 2 * (int)(((long)r * s0) / (2L * S));
+    b = r == S - 1 ? s0 : 2 * (int)(((long)(r + 1) * s0) / (2L * S));
+  };
+  int a, b;
+  fine(rank, a, b);
+  for (int l = 0; l < nlev; ++l) {
+    int minp = 1 << 30;
+    for (int r = 0; r < S; ++r) {
+      int ra, rb;
+      fine(r, ra, rb);
+      for (int k = 0; k < l; ++k) {
+        ra = (ra + 1) / 2;
+        rb = (rb + 1) / 2;
+      }
+      minp = std::min(minp, rb - ra);
+    }
+    if (minp < 2 || l + 1 == nlev) return l;
+    lo[l] = a;
+    hi[l] = b;
+    a = (a + 1) / 2;
+    b = (b + 1) / 2;
+  }
+  return nlev;
 }
 
 static Grid make_grid(int dim, int n) {
@@ -1270,37 +1354,27 @@ static void build(okg_ctx* c) {
     if (coarsest > std::max<int64_t>(p.min_coarse_size, 2000))
       THROW(OKG_ECONFIG,
             "build_hierarchy: coarsest level too large for a direct solve; choose a grid with more factors of two");
-    // slab partition: whole x-planes, even boundaries on the finest
-    // level, coarse ranges by nesting (G owned iff 2G owned); from the first level
-    // where a slab would keep < 2 planes on, levels are replicated on every slab.
+    // slab partition, see slab_partition()
     const int S = c->nslabs;
     c->L_rep = (int)c->lv.size();
     if (S > 1) {
-      const int s0 = c->lv[0].g.s;
-      int a = 2 * (int)(((long)c->rank * s0) / (2L * S)), b = 2 * (int)(((long)(c->rank + 1) * s0) / (2L * S));
-      if (c->rank == S - 1) b = s0;
-      for (size_t l = 0; l < c->lv.size(); ++l) {
-        // smallest slab of this level (same formula for every rank)
-        int minp = 1 << 30;
-        for (int r = 0; r < S; ++r) {
-          int ra = 2 * (int)(((long)r * s0) / (2L * S)), rb = r == S - 1 ? s0 : 2 * (int)(((long)(r + 1) * s0) / (2L * S));
-          for (size_t k = 0; k < l; ++k) {
-            ra = (ra + 1) / 2;
-            rb = (rb + 1) / 2;
-          }
-          minp = std::min(minp, rb - ra);
-        }
-        if (minp < 2 || l + 1 == c->lv.size()) {
-          c->L_rep = (int)l;
-          break;
-        }
-        set_owned(c->lv[l].g, a, b);
-        c->lv[l].gh = 1;
-        a = (a + 1) / 2;
-        b = (b + 1) / 2;
-      }
+      std::vector<int> lo(c->lv.size()), hi(c->lv.size());
+      c->L_rep = slab_partition(c->lv[0].g.s, (int)c->lv.size(), S, c->rank, lo.data(), hi.data());
       if (c->L_rep == 0) THROW(OKG_EINVAL, "slab decomposition: %d slabs leave fewer than 2 planes each", S);
+      for (int l = 0; l < c->L_rep; ++l) {
+        set_owned(c->lv[l].g, lo[l], hi[l]);
+        c->lv[l].gh = 1;
+      }
       for (size_t l = c->L_rep; l < c->lv.size(); ++l) c->lv[l].rep = true;
+      // every slab's restriction range in the first replicated level (allgather_planes)
+      c->rep_lo.assign(S, 0);
+      c->rep_hi.assign(S, 0);
+      for (int r = 0; r < S; ++r) {
+        std::vector<int> rl(c->lv.size()), rh(c->lv.size());
+        slab_partition(c->lv[0].g.s, (int)c->lv.size(), S, r, rl.data(), rh.data());
+        c->rep_lo[r] = (rl[c->L_rep - 1] + 1) / 2;
+        c->rep_hi[r] = (rh[c->L_rep - 1] + 1) / 2;
+      }
     }
     for (size_t l = 0; l < c->lv.size(); ++l) {
       Level& L = c->lv[l];
@@ -1645,6 +1719,7 @@ static void destroy_ctx(okg_ctx* c) {
   if (c->hred) cudaFreeHost(c->hred);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->comm) c->ncl->CommDestroy(c->comm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1790,7 +1865,7 @@ static okg_ctx* slab0(okg_ctx* c) { return c->handle ? c->group->r[0] : c; }
 
 #define SINGLE_SLAB(c, fn)                                                                                    \
   do {                                                                                                        \
-    if ((c)->handle)                                                                                          \
+    if ((c)->handle || (c)->nslabs > 1)                                                                       \
       return fail(OKG_EINVAL, "%s: device-pointer entry point on a %d-slab context (use the host-pointer API)", \
                   fn, (c)->nslabs);                                                                           \
   } while (0)
@@ -1907,6 +1982,82 @@ int okg_create(const okg_params* p, okg_ctx** out) {
   return OKG_OK;
 }
 
+int okg_nccl_unique_id(void* id, size_t len) {
+  if (!id || len < sizeof(ncclUniqueId)) return fail(OKG_EINVAL, "okg_nccl_unique_id: need %zu bytes", sizeof(ncclUniqueId));
+  std::string why;
+  const NcclApi* nc = nccl_api(&why);
+  if (!nc) return fail(OKG_ECUDA, "%s", why.c_str());
+  ncclUniqueId u;
+  const ncclResult_t r = nc->GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(OKG_ECUDA, "ncclGetUniqueId: %s", nc->GetErrorString(r));
+  std::memcpy(id, &u, sizeof u);
+  return OKG_OK;
+}
+
+int okg_create_rank(const okg_params* p, int32_t rank, int32_t nranks, const void* nccl_id, okg_ctx** out) {
+  if (!p || !out) return fail(OKG_EINVAL, "okg_create_rank: null argument");
+  *out = nullptr;
+  if (nranks < 1 || nranks > 16 || rank < 0 || rank >= nranks)
+    return fail(OKG_EINVAL, "okg_create_rank: rank %d of %d", rank, nranks);
+  if (nranks > 1 && !nccl_id) return fail(OKG_EINVAL, "okg_create_rank: %d ranks need an NCCL id", nranks);
+  okg_ctx* c = new okg_ctx();
+  c->p = *p;
+  c->p.nslabs = nranks;
+  c->rank = rank;
+  c->nslabs = nranks;
+  if (nranks > 1) c->p.use_graphs = 0;
+  const int st = guard(nullptr, [&] {
+    CK(cudaSetDevice(p->device));
+    if (nccl_id) {
+      std::string why;
+      c->ncl = nccl_api(&why);
+      if (!c->ncl) THROW(OKG_ECUDA, "%s", why.c_str());
+      ncclUniqueId u;
+      std::memcpy(&u, nccl_id, sizeof u);
+      NCK(c, c->ncl->CommInitRank(&c->comm, nranks, u, rank));
+    }
+    init_ctx(c);
+  });
+  if (st != OKG_OK) {
+    destroy_ctx(c);
+    return st;
+  }
+  *out = c;
+  return OKG_OK;
+}
+
+int okg_slab_partition(int32_t dim, int32_t n, int32_t min_coarse_size, int32_t nslabs, int32_t rank,
+                       int32_t* levels, int32_t* rep_level, int32_t* lo, int32_t* hi) {
+  if ((dim != 2 && dim != 3) || n < 1 || min_coarse_size < 1 || nslabs < 1 || rank < 0 || rank >= nslabs || !levels ||
+      !rep_level || !lo || !hi)
+    return fail(OKG_EINVAL, "okg_slab_partition: bad argument");
+  // build_hierarchy's level count (multigrid.hpp:55-86)
+  int nlev = 0;
+  for (int ln = n;; ln /= 2) {
+    ++nlev;
+    const int64_t s = (int64_t)ln + 1, N = dim == 2 ? s * s : s * s * s;
+    if (!(N > min_coarse_size && ln % 2 == 0) || nlev == 32) break;
+  }
+  *levels = nlev;
+  std::vector<int> l0(nlev, 0), h0(nlev, 0);
+  for (int l = 0; l < nlev; ++l) h0[l] = (n >> l) + 1;  // one slab / replicated level: every plane
+  int rep = nlev;
+  if (nslabs > 1) {
+    rep = slab_partition(n + 1, nlev, nslabs, rank, l0.data(), h0.data());
+    if (rep == 0) return fail(OKG_EINVAL, "slab decomposition: %d slabs leave fewer than 2 planes each", nslabs);
+    for (int l = rep; l < nlev; ++l) {
+      l0[l] = 0;
+      h0[l] = (n >> l) + 1;
+    }
+  }
+  *rep_level = rep;
+  for (int l = 0; l < nlev; ++l) {
+    lo[l] = l0[l];
+    hi[l] = h0[l];
+  }
+  return OKG_OK;
+}
+
 void okg_destroy(okg_ctx* c) {
   if (c && c->handle) destroy_handle(c);
   else destroy_ctx(c);
@@ -1935,13 +2086,22 @@ int okg_get_info(okg_ctx* h, okg_info* info) {
   info->tail_start = c->tail_start;
   for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
     if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
-  info->nslabs = h->handle ? h->nslabs : 1;
+  info->nslabs = h->handle ? h->nslabs : c->nslabs;
   info->rep_level = std::min<int>(c->L_rep, (int)c->lv.size());
+  if (h->handle)
+    for (okg_ctx* s : h->group->r) info->device_bytes += static_cast<int64_t>(s->bytes);
+  else
+    info->device_bytes = static_cast<int64_t>(c->bytes);  // this process's slab
   for (int r = 0; r < info->nslabs; ++r) {
-    okg_ctx* s = h->handle ? h->group->r[r] : h;
-    info->device_bytes += static_cast<int64_t>(s->bytes);
-    info->slab_ilo[r] = s->fine.ilo;
-    info->slab_ihi[r] = s->fine.ihi;
+    std::vector<int> lo(c->lv.size()), hi(c->lv.size());
+    if (info->nslabs > 1) {
+      slab_partition(c->lv[0].g.s, (int)c->lv.size(), info->nslabs, r, lo.data(), hi.data());
+    } else {
+      lo[0] = 0;
+      hi[0] = c->lv[0].g.s;
+    }
+    info->slab_ilo[r] = lo[0];
+    info->slab_ihi[r] = hi[0];
   }
   return OKG_OK;
 }
@@ -2226,7 +2386,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
   Level& L0 = c->lv[0];
   const Grid& g = L0.g;
   const double om = c->p.mg_omega;
-  const double N = (double)g.N;
+  const double N = (double)(g.hi - g.lo);  // owned vertices (the whole level on one slab)
   const double B = 8.0;
   // operands: reuse workspace vectors (contents are finite)
   double *x = c->cd0, *b = c->cd1, *y = c->cr, *z = c->kv;
@@ -2244,7 +2404,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
       case OKG_KT_PRE2:
         if (T) tiled<DIM, L_JAC0, T_JACOBI>(c, L0, L0.shat, targs(b, b, y, nullptr, om));
         else {
-          launch(c, k_pre2<DIM>, nblk(g.N), BS, 0, g, dev_op<DIM>(L0.shat), b, y, om);
+          launch(c, k_pre2<DIM>, own(g), BS, 0, g, dev_op<DIM>(L0.shat), b, y, om);
           note(c);
         }
         break;
@@ -2261,14 +2421,14 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
           a.c2 = c->cheb_c2[0];
           tiled<DIM, L_PLAIN, T_CHEB>(c, L0, c->A, a);
         } else {
-          launch(c, k_cheb_step<DIM>, nblk(g.N), BS, 0, g, dev_op<DIM>(c->A), x, b, y, c->zz, c->rr, z,
+          launch(c, k_cheb_step<DIM>, own(g), BS, 0, g, dev_op<DIM>(c->A), x, b, y, c->zz, c->rr, z,
                                                             c->cheb_c1[0], c->cheb_c2[0], 0);
           note(c);
         }
         break;
       case OKG_KT_JACOBIAN: jacobian<DIM>(c, c->pz, c->pw); break;
       case OKG_KT_RESTRICT:
-        launch(c, k_restrict<DIM>, nblk(c->lv[1].g.N), BS, 0, g, c->lv[1].g, x, c->lv[1].b);
+        launch(c, k_restrict<DIM>, own(c->lv[1].g), BS, 0, g, c->lv[1].g, x, c->lv[1].b);
         note(c);
         break;
       case OKG_KT_PROLONG:
@@ -2278,7 +2438,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
           a.gc = c->lv[1].g;
           tiled<DIM, L_PROLONG, T_JACOBI>(c, L0, L0.shat, a);
         } else {
-          launch(c, k_prolong_add<DIM>, nblk(g.N), BS, 0, g, c->lv[1].g, c->lv[1].x, y);
+          launch(c, k_prolong_add<DIM>, own(g), BS, 0, g, c->lv[1].g, c->lv[1].x, y);
           note(c);
         }
         break;
@@ -2287,7 +2447,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
   };
   if ((which == OKG_KT_RESTRICT || which == OKG_KT_PROLONG) && c->lv.size() < 2)
     THROW(OKG_EINVAL, "okg_kernel_timing: single-level hierarchy");
-  const double Nc = c->lv.size() > 1 ? (double)c->lv[1].g.N : 0.0;
+  const double Nc = c->lv.size() > 1 ? (double)(c->lv[1].g.hi - c->lv[1].g.lo) : 0.0;
   const double npos = Traits<DIM>::NPOS + 1;
   switch (which) {
     case OKG_KT_SMOOTH: case OKG_KT_RESID: *bytes = 3 * N * B; break;
@@ -2319,7 +2479,7 @@ extern "C" {
 
 int okg_kernel_timing(okg_ctx* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {
   if (!c || !avg_ms || !bytes || reps < 1) return fail(OKG_EINVAL, "okg_kernel_timing: bad argument");
-  SINGLE_SLAB(c, "okg_kernel_timing");
+  if (c->handle) return fail(OKG_EINVAL, "okg_kernel_timing: time one slab (okg_create_rank) instead");
   return guard(c, [&] { DISPATCH(c, kernel_timing_impl, c, which, reps, avg_ms, bytes); });
 }
 

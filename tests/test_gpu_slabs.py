@@ -182,3 +182,31 @@ def test_full_size_3d128_two_slabs():
         ctx.close()
     assert out[0][0] == out[1][0] and out[0][1] == out[1][1]
     assert relerr(out[1][2].u, out[0][2].u) <= 1e-10
+
+
+def test_rank_context_one_process():
+    """okg_create_rank (one process per GPU, NCCL transport) with a single rank: a
+    real NCCL communicator is created; results equal the ordinary context."""
+    cfg = cfg_for(2, 64)
+    one = okg.SchurContext(cfg)
+    r0 = okg.SchurContext(cfg, rank=0, nranks=1, nccl_id=okg.nccl_unique_id())
+    assert r0.nslabs == 1 and r0.slab_planes == [(0, 65)]
+    N = one.n
+    st0 = okg.State(okg.seeded_ic(N, 2, 0.0), np.zeros(N))
+    out = []
+    for ctx in (one, r0):
+        ctx.set_state(st0)
+        s = ctx.step_resident()
+        out.append((s.newton_iters, s.gmres_iters, ctx.get_state()))
+    assert out[0][:2] == out[1][:2]
+    assert np.array_equal(out[0][2].u, out[1][2].u)
+    r0.close()
+    one.close()
+
+
+def test_create_rank_argument_checks():
+    cfg = cfg_for(2, 64)
+    with pytest.raises(okg.InvalidArgument):
+        okg.SchurContext(cfg, rank=2, nranks=2, nccl_id=bytes(128))
+    with pytest.raises(okg.InvalidArgument):
+        okg.SchurContext(cfg, rank=0, nranks=2, nccl_id=None)
