@@ -61,9 +61,11 @@ typedef struct okg_params {
   int32_t use_graphs;       /* capture the Arnoldi operator in a CUDA graph (default 1) */
   int32_t tiled_min_n;      /* levels with n >= this use the shared-memory tiled stencil
                                kernels; 0 = default (3D: 32, 2D: 128), < 0 = never */
-  int32_t tail_max_vertices;/* multigrid levels (below the finest) with at most this many
-                               vertices run as ONE single-CTA V-cycle kernel;
-                               0 = default (never), > 0 = threshold */
+  int32_t tail_max_vertices;/* from the first level (below the finest) with at most this
+                               many vertices down to the coarsest, the V-cycle runs as ONE
+                               thread-block-cluster kernel (shared-memory resident, 3D
+                               n <= 16, 2D n <= 64); 0 = default (3D 1000, 2D 1100),
+                               < 0 = never */
   int32_t disable_pdl;      /* 1: launch without programmatic dependent launch */
   int32_t mg_fuse;          /* temporally blocked V(2,2) level kernels (one "down" and one
                                "up" launch per level): 0 = default (2D: every level
@@ -75,6 +77,8 @@ typedef struct okg_params {
                                the order of the cross-slab reduction sums. */
   int32_t slab_devices;     /* 0: every slab on `device` (1-GPU emulation); 1: slab r on
                                device `device + r` (peer copies over NVLink) */
+  int32_t tail_cluster;     /* CTAs in the tail's cluster (they split the rows of the dense
+                               coarse inverse): 0 = default (enough for <= 96 KB each), 1..16 */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -110,11 +114,12 @@ typedef struct okg_info {
   double c, sqrt_c, a_coeff, dt_theta, lambda_lo, lambda_hi, eps_sqrt_c;
   int64_t device_bytes;       /* device memory held by the context        */
   int32_t graph_nodes;        /* kernels in the captured Arnoldi graph    */
-  int32_t tail_start;         /* first level of the single-CTA tail (-1: none) */
+  int32_t tail_start;         /* first level of the cluster tail (-1: none) */
   int32_t tiled_mask;         /* bit l set: level l uses the tiled kernels */
   int32_t nslabs;             /* slabs of the decomposition (1: none)      */
   int32_t rep_level;          /* first level replicated on every slab (levels if none) */
   int32_t slab_ilo[16], slab_ihi[16]; /* owned x-planes [ilo, ihi) of the finest level per slab */
+  int32_t tail_cluster;       /* CTAs in the tail's thread-block cluster */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */

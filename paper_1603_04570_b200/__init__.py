@@ -71,7 +71,8 @@ class SolverConfig:
 
     def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
                   tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
-                  mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False) -> _lib.Params:
+                  mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
+                  tail_cluster: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -87,6 +88,7 @@ class SolverConfig:
         p.mg_fuse = mg_fuse
         p.nslabs = nslabs
         p.slab_devices = 1 if slab_devices else 0
+        p.tail_cluster = tail_cluster
         return p
 
     def validate(self) -> None:
@@ -253,7 +255,8 @@ class SchurContext:
     def __init__(self, cfg: SolverConfig, device: int = 0, shat_perturb: float = 0.0,
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
                  pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
-                 rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None):
+                 rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None,
+                 tail_cluster: int = 0):
         """nslabs > 1: x-plane slab decomposition, one host thread + stream per
         slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
         `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
@@ -265,7 +268,7 @@ class SchurContext:
         self.device = device
         self.handle = C.c_void_p()
         params = cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl, mg_fuse,
-                               nslabs, slab_devices)
+                               nslabs, slab_devices, tail_cluster)
         if rank is None:
             check(lib.okg_create(C.byref(params), C.byref(self.handle)))
         else:
@@ -290,6 +293,7 @@ class SchurContext:
         self.device_bytes = int(info.device_bytes)
         self.graph_nodes = int(info.graph_nodes)
         self.tail_start = int(info.tail_start)
+        self.tail_cluster = int(info.tail_cluster)
         self.tiled_levels = [l for l in range(self.levels) if (info.tiled_mask >> l) & 1]
         self.nslabs = int(info.nslabs)
         self.rep_level = int(info.rep_level)

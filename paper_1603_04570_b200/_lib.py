@@ -45,6 +45,7 @@ class Params(C.Structure):
         ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
         ("tail_max_vertices", C.c_int32), ("disable_pdl", C.c_int32),
         ("mg_fuse", C.c_int32), ("nslabs", C.c_int32), ("slab_devices", C.c_int32),
+        ("tail_cluster", C.c_int32),
     ]
 
 
@@ -73,7 +74,7 @@ class Info(C.Structure):
         ("eps_sqrt_c", C.c_double), ("device_bytes", C.c_int64), ("graph_nodes", C.c_int32),
         ("tail_start", C.c_int32), ("tiled_mask", C.c_int32),
         ("nslabs", C.c_int32), ("rep_level", C.c_int32),
-        ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16),
+        ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16), ("tail_cluster", C.c_int32),
     ]
 
 

@@ -121,7 +121,9 @@ struct okg_ctx {
   std::vector<Level> lv;
   int nc = 0;
   double* Ainv = nullptr;
-  int tail_start = -1;  // first level run by the single-CTA tail kernel (-1: none)
+  int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
+  int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
+  double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
   double b_int = 0;
   double* b_tab = nullptr;
   Nonlin nl;
@@ -220,6 +222,28 @@ static void launch(okg_ctx* c, void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
   if (e != cudaSuccess) THROW(OKG_ECUDA, "cudaLaunchKernelEx: %s", cudaGetErrorString(e));
+}
+
+// one thread-block cluster of `csize` CTAs (k_vcycle_tail), PDL as above
+template <class... KArgs, class... Args>
+static void launch_cluster(okg_ctx* c, void (*kernel)(KArgs...), unsigned csize, dim3 block, size_t smem,
+                           Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = c->p.disable_pdl ? 0 : 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = csize;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = csize > 1 ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) THROW(OKG_ECUDA, "cudaLaunchKernelEx (cluster %u): %s", csize, cudaGetErrorString(e));
 }
 
 static unsigned nblk(size_t n) { return static_cast<unsigned>((n + BS - 1) / BS); }
@@ -606,30 +630,53 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
   note(c);
 }
 
-// levels tail_start..coarsest in one single-CTA launch (okg_tail.cuh)
+// levels tail_start..coarsest in one launch (okg_tail.cuh)
+template <int DIM, int N0>
+static size_t tail_smem(int nc, int csize) {
+  const int rows = (nc + csize - 1) / csize;
+  return sizeof(double) * ((size_t)tail_smem_doubles<DIM, N0>() + TL<DIM, N0>::N + (size_t)rows * nc);
+}
+
+template <int DIM, int N0>
+static void tail_launch(okg_ctx* c, const TailArgs<DIM>& A) {
+  launch_cluster(c, k_vcycle_tail<DIM, N0>, (unsigned)c->tail_cluster, TAIL_NT, tail_smem<DIM, N0>(c->nc, c->tail_cluster),
+                 A);
+}
+
+// per instantiation: opt in to the shared memory / cluster size it needs
+template <int DIM, int N0>
+static void tail_prepare(okg_ctx* c) {
+  CK(cudaFuncSetAttribute(k_vcycle_tail<DIM, N0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)tail_smem<DIM, N0>(c->nc, c->tail_cluster)));
+  if (c->tail_cluster > 8)
+    CK(cudaFuncSetAttribute(k_vcycle_tail<DIM, N0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+template <int DIM, class F>
+static void tail_dispatch(int n0, F&& f) {
+  switch (n0) {
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    case 16: f(std::integral_constant<int, 16>{}); break;
+    case 32: if constexpr (DIM == 2) f(std::integral_constant<int, 32>{}); break;
+    case 64: if constexpr (DIM == 2) f(std::integral_constant<int, 64>{}); break;
+    default: THROW(OKG_EOTHER, "tail: unsupported first level n = %d", n0);
+  }
+}
+
 template <int DIM>
 static void run_tail(okg_ctx* c, int l0, const double* rhs, double* out) {
   TailArgs<DIM> A;
   std::memset(&A, 0, sizeof A);
+  A.tabs = c->tail_tab;
   A.nl = static_cast<int>(c->lv.size()) - l0;
-  for (int q = 0; q < A.nl; ++q) {
-    Level& L = c->lv[l0 + q];
-    A.L[q].g = L.g;
-    A.L[q].op = dev_op<DIM>(L.shat);
-    A.L[q].b = L.b;
-    A.L[q].x = L.x;
-    A.L[q].ea = L.ea;
-    A.L[q].eb = L.eb;
-    A.L[q].res = L.res;
-  }
-  A.pre = c->p.mg_pre;
-  A.post = c->p.mg_post;
   A.omega = c->p.mg_omega;
   A.rhs = rhs;
   A.out = out;
   A.Ainv = c->Ainv;
   A.nc = c->nc;
-  launch(c, k_vcycle_tail<DIM>, 1, TAIL_NT, 0, A);
+  tail_dispatch<DIM>(c->lv[l0].g.n, [&](auto N0) { tail_launch<DIM, decltype(N0)::value>(c, A); });
   note(c);
 }
 
@@ -1392,14 +1439,54 @@ static void build(okg_ctx* c) {
     c->foff = ((ptrdiff_t)c->fine.ilo - c->lv[0].gh) * c->fine.ps;
     c->seg = Seg{(size_t)c->lv[0].gh * c->fine.ps, (size_t)(c->fine.hi - c->fine.lo), c->B};
     c->N2 = 2 * c->B;
-    // single-CTA tail for the small levels (okg_tail.cuh); single slab only
-    const int64_t tmax = p.tail_max_vertices;
-    if (tmax > 0 && S == 1) {
-      for (size_t l = 1; l < c->lv.size(); ++l)
-        if ((int64_t)c->lv[l].g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL) {
-          c->tail_start = (int)l;
-          break;
+    // shared-memory tail for the small levels (okg_tail.cuh): from the first level
+    // with n <= tail_max_n (and at most tail_max_vertices vertices when > 0) down to
+    // the coarsest, in one launch; V(2,2) only, not on levels split across slabs
+    // default depth: the 9^3 (3D) / 33^2 (2D) level -- measured: one SM beats the
+    // multi-CTA level kernels only where a level is a few hundred to ~1000 vertices
+    const int64_t tmax = p.tail_max_vertices == 0 ? (DIM == 3 ? 1000 : 1100) : p.tail_max_vertices;
+    if (p.tail_max_vertices >= 0 && p.mg_pre == 2 && p.mg_post == 2) {
+      const int ncv = (int)c->lv.back().g.N;
+      for (size_t l = 1; l + 1 < c->lv.size(); ++l) {
+        const Level& L = c->lv[l];
+        if (!(L.g.n <= tail_max_n<DIM>() && (int64_t)L.g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL &&
+              (S == 1 || (int)l >= c->L_rep)))
+          continue;
+        // cluster size: split the coarse inverse so each CTA stages <= 96 KB of it
+        int C = 1;
+        while (C < 16 && (size_t)((ncv + C - 1) / C) * ncv * sizeof(double) > 96 * 1024) C *= 2;
+        C = std::min(std::max(C, p.tail_cluster > 0 ? p.tail_cluster : 1), 16);
+        size_t need = 0;
+        tail_dispatch<DIM>(L.g.n, [&](auto N0) { need = tail_smem<DIM, decltype(N0)::value>(ncv, C); });
+        if (need > 220 * 1024) continue;  // shared-memory budget: try a deeper level
+        c->tail_start = (int)l;
+        c->tail_cluster = C;
+        break;
+      }
+    }
+    if (c->tail_start > 0) {
+      // tables: every tail level's class rows, then the restriction weights
+      const int NO = Traits<DIM>::NOFF, NCL = Traits<DIM>::NCLS;
+      std::vector<double> tt((size_t)tail_table_doubles<DIM>(), 0.0);
+      for (size_t q = 0; q + c->tail_start < c->lv.size(); ++q) {
+        const std::vector<double>& h = c->lv[c->tail_start + q].shat.htab;
+        std::copy(h.begin(), h.end(), tt.begin() + q * NCL * (NO + 1));
+      }
+      for (int cl = 0; cl < NCL; ++cl)
+        for (int o = 0; o < NO; ++o) {
+          bool ok = true;
+          int cc = cl;
+          for (int d = DIM - 1; d >= 0; --d) {
+            const int cd = cc % 3, od = off_comp(DIM, o, d);
+            cc /= 3;
+            ok = ok && !(cd == 0 && od < 0) && !(cd == 2 && od > 0);
+          }
+          tt[(size_t)TAIL_MAXL * NCL * (NO + 1) + cl * NO + o] = ok ? (o == NO / 2 ? 1.0 : 0.5) : 0.0;
         }
+      c->tail_tab = dalloc(c, tt.size());
+      CK(cudaMemcpyAsync(c->tail_tab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      c->nc = (int)c->lv.back().g.N;
+      tail_dispatch<DIM>(c->lv[c->tail_start].g.n, [&](auto N0) { tail_prepare<DIM, decltype(N0)::value>(c); });
     }
     // temporally blocked down/up kernels for V(2,2) (okg_vcycle.cuh)
     // default: every coarse level in 2D; in 3D the levels with n <= 32 (the halo-3
@@ -2084,6 +2171,7 @@ int okg_get_info(okg_ctx* h, okg_info* info) {
   info->eps_sqrt_c = c->eps_sqrt_c;
   info->graph_nodes = c->arn_nodes;
   info->tail_start = c->tail_start;
+  info->tail_cluster = c->tail_start > 0 ? c->tail_cluster : 0;
   for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
     if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
   info->nslabs = h->handle ? h->nslabs : c->nslabs;

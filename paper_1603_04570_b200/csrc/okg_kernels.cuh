@@ -23,7 +23,6 @@
 
 #include "okg_common.cuh"
 #include "okg_tiled.cuh"
-#include "okg_tail.cuh"
 
 namespace okg {
 
@@ -721,3 +720,4 @@ __global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ 
 
 #include "okg_tiled_c.cuh"
 #include "okg_vcycle.cuh"
+#include "okg_tail.cuh"  // uses slot_ok / op_row above

@@ -342,13 +342,17 @@ def test_solver_knobs_match_oracle(port_lib, kw, dim, n, mode):
     ctx.close()
 
 
-@pytest.mark.parametrize("dim,n", [(2, 64), (3, 32), (3, 16)])
+@pytest.mark.parametrize("dim,n", [(2, 64), (2, 256), (3, 32), (3, 16), (3, 64)])
 def test_fused_vcycle_bit_identical(dim, n):
     # okg_vcycle.cuh claims the same arithmetic per vertex as the unfused kernels
     cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, min_coarse_size=10)
     rng = np.random.default_rng(5)
     outs = []
-    for mode in (dict(mg_fuse=-1), dict(mg_fuse=1), dict(mg_fuse=0)):
+    big = 1 << 30
+    for mode in (dict(mg_fuse=-1, tail_max_vertices=-1), dict(mg_fuse=1, tail_max_vertices=-1),
+                 dict(mg_fuse=0, tail_max_vertices=-1), dict(mg_fuse=0),
+                 dict(tail_max_vertices=big, tail_cluster=16), dict(tail_max_vertices=big, tail_cluster=1),
+                 dict(tail_max_vertices=big, tail_cluster=4), dict(tail_max_vertices=2000, tail_cluster=8)):
         ctx = okg.SchurContext(cfg, **mode)
         x = rng.uniform(-1, 1, ctx.n) if not outs else outs[0][0]
         outs.append((x, ctx.apply(_lib.OP_VCYCLE, x), ctx.apply(_lib.OP_SHAT_INV, x)))

@@ -4,7 +4,7 @@
 // kernel variants differ in data movement, not in boundary handling).
 // Prints GB/s of 24 algorithmic bytes per vertex.  Not part of the product.
 //
-// nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/sb tools/stencil_bench.cu
+// nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -o tools/stencil_bench tools/stencil_bench.cu
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -211,6 +211,120 @@ __global__ void __launch_bounds__(256) v3_zrun(G3 g, const double* __restrict__ 
   }
 }
 
+
+// ---------------- cp.async helpers ----------------
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = ok ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(ok ? gmem : smem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ---------------- V4: whole-tile staging by cp.async (no register staging) ----------------
+template <int TK, int TJ, int TI, int MINB>
+__global__ void __launch_bounds__(TK* TJ, MINB) v4_tile_async(G3 g, const double* __restrict__ x,
+                                                               const double* __restrict__ b, double* __restrict__ y,
+                                                               int ktiles, int jtiles) {
+  constexpr int NT = TK * TJ, PW = TK + 2, PSZ = PW * (TJ + 2);
+  extern __shared__ double tile[];
+  int bb = blockIdx.x;
+  const int kt = bb % ktiles;
+  bb /= ktiles;
+  const int jt = bb % jtiles, ic = bb / jtiles;
+  const int k0 = 1 + kt * TK, j0 = 1 + jt * TJ, i0 = 1 + ic * TI;
+  const int ni = min(TI, g.n - i0);
+  const int tid = threadIdx.x, tk = tid % TK, tj = tid / TK;
+  const int total = (ni + 2) * PSZ;
+  for (int e = tid; e < total; e += NT) {
+    const int p = e / PSZ, r = e - p * PSZ, hj = r / PW, hk = r - hj * PW;
+    const int gj = j0 - 1 + hj, gk = k0 - 1 + hk;
+    const bool ok = gj <= g.n && gk <= g.n;
+    cp_async8(tile + e, x + (unsigned)(i0 - 1 + p) * g.ps + gj * g.s + gk, ok);
+  }
+  cp_commit();
+  const int k = k0 + tk, j = j0 + tj;
+  const bool active = k < g.n && j < g.n;
+  double pb[TI];
+  const unsigned idx0 = (unsigned)i0 * g.ps + j * g.s + k;
+#pragma unroll
+  for (int t = 0; t < TI; ++t) pb[t] = (active && t < ni) ? b[idx0 + t * g.ps] : 0.0;
+  cp_wait<0>();
+  __syncthreads();
+  if (!active) return;
+#pragma unroll
+  for (int t = 0; t < TI; ++t) {
+    double s = 0.0, own = 0.0;
+#pragma unroll
+    for (int o = 0; o < 15; ++o) {
+      const double v = tile[(t + 1 + OFF3[o][0]) * PSZ + (tj + 1 + OFF3[o][1]) * PW + tk + 1 + OFF3[o][2]];
+      if (o == 7) own = v;
+      s = fma(cw[o], v, s);
+    }
+    if (t < ni) y[idx0 + t * g.ps] = own + OMEGA_INVD * (pb[t] - s);
+  }
+}
+
+// ---------------- V5: x-marching, cp.async ring of 8 planes, PD planes prefetched ----------------
+template <int TK, int TJ, int CH, int PD, int MINB>
+__global__ void __launch_bounds__(TK* TJ, MINB) v5_march_async(G3 g, const double* __restrict__ x,
+                                                                const double* __restrict__ b, double* __restrict__ y,
+                                                                int ktiles, int jtiles) {
+  constexpr int NT = TK * TJ, PW = TK + 2, PSZ = PW * (TJ + 2);
+  constexpr int RPT = (PSZ + NT - 1) / NT;
+  extern __shared__ double sm[];
+  double* ring = sm;              // [8][PSZ]
+  double* bring = sm + 8 * PSZ;   // [8][NT]
+  int bb = blockIdx.x;
+  const int kt = bb % ktiles;
+  bb /= ktiles;
+  const int jt = bb % jtiles, ic = bb / jtiles;
+  const int k0 = 1 + kt * TK, j0 = 1 + jt * TJ, i0 = 1 + ic * CH;
+  const int i1 = min(i0 + CH, g.n);
+  const int tid = threadIdx.x, tk = tid % TK, tj = tid / TK;
+  const int k = k0 + tk, j = j0 + tj;
+  const bool active = k < g.n && j < g.n;
+  unsigned off[RPT];
+  bool ok[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = tid + q * NT;
+    const int hj = r / PW, hk = r - hj * PW;
+    const int gj = j0 - 1 + hj, gk = k0 - 1 + hk;
+    ok[q] = r < PSZ && gj <= g.n && gk <= g.n;
+    off[q] = ok[q] ? gj * g.s + gk : 0;
+  }
+  const unsigned own_off = active ? (unsigned)j * g.s + k : 0;
+  auto issue = [&](int ip) {  // plane ip of x (+ b at plane ip when it is computed)
+    if (ip <= i1) {
+      double* dst = ring + (ip & 7) * PSZ;
+#pragma unroll
+      for (int q = 0; q < RPT; ++q)
+        if (tid + q * NT < PSZ) cp_async8(dst + tid + q * NT, x + (unsigned)ip * g.ps + off[q], ok[q]);
+      if (ip >= i0 && ip < i1) cp_async8(bring + (ip & 7) * NT + tid, b + (unsigned)ip * g.ps + own_off, active);
+    }
+    cp_commit();  // always commit (empty groups keep the wait count uniform)
+  };
+  issue(i0 - 1);
+  for (int d = 0; d <= PD; ++d) issue(i0 + d);
+  for (int i = i0; i < i1; ++i) {
+    cp_wait<PD>();  // planes <= i+1 landed
+    __syncthreads();
+    if (active) {
+      double s = 0.0, own = 0.0;
+#pragma unroll
+      for (int o = 0; o < 15; ++o) {
+        const double v = ring[((i + OFF3[o][0]) & 7) * PSZ + (tj + 1 + OFF3[o][1]) * PW + tk + 1 + OFF3[o][2]];
+        if (o == 7) own = v;
+        s = fma(cw[o], v, s);
+      }
+      y[(unsigned)i * g.ps + own_off] = own + OMEGA_INVD * (bring[(i & 7) * NT + tid] - s);
+    }
+    issue(i + PD + 1);
+  }
+}
+
 __global__ void triad(const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, size_t n) {
   for (size_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += (size_t)gridDim.x * 256) y[i] = x[i] + 0.5 * b[i];
 }
@@ -387,6 +501,39 @@ int run(int n, bool extras) {
     report(nm, ms);                                                                            \
   }
   V3(2) V3(4) V3(8)
+#define V4(TK, TJ, TI, MINB)                                                                                  \
+  {                                                                                                          \
+    const int kt = (n - 1 + TK - 1) / TK, jt = (n - 1 + TJ - 1) / TJ, it = (n - 1 + TI - 1) / TI;             \
+    const size_t sm = (size_t)(TI + 2) * (TK + 2) * (TJ + 2) * 8;                                             \
+    CK(cudaFuncSetAttribute(v4_tile_async<TK, TJ, TI, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    float ms = timeit(                                                                                       \
+        [&] {                                                                                                \
+          int q = rot++ % NSET;                                                                              \
+          v4_tile_async<TK, TJ, TI, MINB><<<kt * jt * it, TK * TJ, sm>>>(g, x[q], b[q], y[q], kt, jt);       \
+        },                                                                                                   \
+        reps);                                                                                               \
+    char nm[64];                                                                                             \
+    snprintf(nm, 64, "v4 async tile %dx%dx%d m%d", TK, TJ, TI, MINB);                                        \
+    report(nm, ms);                                                                                          \
+  }
+  V4(32, 8, 4, 1) V4(32, 8, 4, 6) V4(32, 8, 8, 4) V4(32, 4, 4, 8) V4(32, 8, 2, 8)
+#define V5(TK, TJ, CH, PD, MINB)                                                                              \
+  {                                                                                                          \
+    const int kt = (n - 1 + TK - 1) / TK, jt = (n - 1 + TJ - 1) / TJ, it = (n - 1 + CH - 1) / CH;             \
+    const size_t sm = (size_t)8 * ((TK + 2) * (TJ + 2) + TK * TJ) * 8;                                       \
+    CK(cudaFuncSetAttribute(v5_march_async<TK, TJ, CH, PD, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    float ms = timeit(                                                                                       \
+        [&] {                                                                                                \
+          int q = rot++ % NSET;                                                                              \
+          v5_march_async<TK, TJ, CH, PD, MINB><<<kt * jt * it, TK * TJ, sm>>>(g, x[q], b[q], y[q], kt, jt);  \
+        },                                                                                                   \
+        reps);                                                                                               \
+    char nm[64];                                                                                             \
+    snprintf(nm, 64, "v5 march async %dx%d ch%d pd%d", TK, TJ, CH, PD);                                     \
+    report(nm, ms);                                                                                          \
+  }
+  V5(32, 8, 8, 2, 4) V5(32, 8, 16, 2, 4) V5(32, 8, 16, 4, 4) V5(32, 8, 32, 4, 4) V5(32, 4, 16, 4, 8)
+  V5(32, 4, 32, 4, 8) V5(64, 4, 16, 3, 4) V5(32, 8, 16, 6, 4) V5(32, 4, 8, 3, 8)
   if (extras) {
     // PDL: chains of 200 dependent launches
     const int kt = (n - 1 + 31) / 32, jt = (n - 1 + 7) / 8, it = (n - 1 + 3) / 4;
