@@ -158,8 +158,6 @@ __device__ void tail_level(const TailArgs<DIM>& A, const double* tabs, double* b
     const int nc = A.nc;
     const int r0 = (int)(rk * nc / C), r1 = (int)((rk + 1) * nc / C);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    cpa_wait<0>();  // this CTA's rows of A_c^{-1} (staged at kernel entry)
-    __syncthreads();
     for (int row = r0 + warp; row < r1; row += TAIL_NT / 32) {
       double s = 0.0;
       const double* a = ainv + (size_t)(row - r0) * nc;
@@ -247,7 +245,6 @@ __host__ __device__ inline int tail_rows(int nc, int C, int rk) { return (rk + 1
 
 template <int DIM, int N0>
 __global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> A) {
-  PDL_ENTRY();
   extern __shared__ double sm[];
   namespace cg = cooperative_groups;
   const unsigned C = cg::this_cluster().num_blocks(), rk = cg::this_cluster().block_rank();
@@ -257,10 +254,10 @@ __global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> 
   double* rhs0 = tabs + NTAB;
   double* base = rhs0 + N0V;
   double* ainv = base + tail_levels_doubles<DIM, N0, 0>();
-  // group 0: tables + rhs (needed now); group 1: this rank's rows of A_c^{-1} (needed
-  // at the coarsest level -- the copy overlaps the down sweep)
+  // constants first -- tables (group 0) and this rank's rows of A_c^{-1} (group 1) do
+  // not depend on the predecessor kernel, so they are issued before
+  // griddepcontrol.wait and overlap its tail; then the rhs (group 2)
   for (int e = threadIdx.x; e < NTAB; e += TAIL_NT) cpa8(tabs + e, A.tabs + e);
-  for (int e = threadIdx.x; e < N0V; e += TAIL_NT) cpa8(rhs0 + e, A.rhs + e);
   cpa_commit();
   {
     const int r0 = (int)(rk * A.nc / C);
@@ -270,7 +267,10 @@ __global__ void __launch_bounds__(TAIL_NT, 1) k_vcycle_tail(const TailArgs<DIM> 
   }
   cpa_commit();
   tail_zero_guards<DIM, N0, 0>(base);
-  cpa_wait<1>();
+  PDL_ENTRY();
+  for (int e = threadIdx.x; e < N0V; e += TAIL_NT) cpa8(rhs0 + e, A.rhs + e);
+  cpa_commit();
+  cpa_wait<0>();  // (the coarse inverse is small enough to wait for here)
   __syncthreads();
   tail_level<DIM, N0, 0>(A, tabs, base, ainv, [&](int u) { return rhs0[u]; }, A.out, rk == 0);
   // no CTA may exit while another still reads its shared memory (coarse rows)

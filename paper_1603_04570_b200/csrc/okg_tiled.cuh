@@ -30,12 +30,14 @@ struct TileCfg<3> {
   static constexpr int TK = 32, TJ = 8, NT = TK * TJ;
   static constexpr int PW = TK + 2, PH = TJ + 2, PSZ = PW * PH;
   static constexpr int MINB = 6;  // CTAs per SM the register budget must allow
+  static constexpr int MINB_C = 3;  // same for the C-block kernels (okg_tiled_c.cuh)
 };
 template <>
 struct TileCfg<2> {
   static constexpr int TK = 256, TJ = 1, NT = TK * TJ;
   static constexpr int PW = TK + 2, PH = 1, PSZ = PW;
   static constexpr int MINB = 4;
+  static constexpr int MINB_C = 4;
 };
 
 struct Tiling {

@@ -93,7 +93,7 @@ __device__ __forceinline__ void c_vertex(const Grid& g, const Op<DIM>& Mop, cons
 }
 
 template <int DIM, int MODE, int TI>
-__global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled_c(Grid g, Op<DIM> Mop, Op<DIM> Kop, Op<DIM> Aop,
+__global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB_C) k_tiled_c(Grid g, Op<DIM> Mop, Op<DIM> Kop, Op<DIM> Aop,
                                                               Tiling tl, CTArgs a, Reduce red) {
   PDL_ENTRY();
   using TC = TileCfg<DIM>;

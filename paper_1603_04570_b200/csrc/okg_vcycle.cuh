@@ -81,40 +81,49 @@ __device__ __forceinline__ uint32_t lin_of(const Grid& g, int i, int j, int k) {
   return DIM == 3 ? (uint32_t)i * g.ps + (uint32_t)j * g.s + k : (uint32_t)i * g.s + k;
 }
 
-// A s at vertex (i,j,k) of class cls, s read from region buffer `src` (region rs)
+// A s at vertex (i,j,k) of class cls, s read from region buffer `src` (region rs).
+// W = the level's class table in shared memory ([NCLS][NOFF+1], missing slots 0):
+// every vertex runs the same NOFF taps (the staged region is zero outside the
+// grid); vs the unfused kernels, which skip zero-weight slots of boundary rows,
+// only the sign of a zero can differ.
 template <int DIM, class RS>
-__device__ __forceinline__ double reg_row(const Op<DIM>& op, int cls, const double* src, const RS& rs, int i, int j,
+__device__ __forceinline__ double reg_row(const double* W, int cls, const double* src, const RS& rs, int i, int j,
                                           int k, double& own) {
   constexpr int NO = Traits<DIM>::NOFF;
   const int c = rs.index(i, j, k);
   constexpr int sj = DIM == 3 ? RS::NK : 0, si = DIM == 3 ? RS::NJ * RS::NK : RS::NK;
+  const double* w = W + cls * (NO + 1);
   double As = 0.0;
-  if (cls == Traits<DIM>::INTERIOR) {
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const int di = off_comp(DIM, o, 0), dj = DIM == 3 ? off_comp(DIM, o, 1) : 0, dk = off_comp(DIM, o, DIM - 1);
-      const double v = src[c + di * si + dj * sj + dk];
-      if (o == Traits<DIM>::CENTER) own = v;
-      As = fma(op.w[o], v, As);
-    }
-  } else {
-    const double* w = op.tab + cls * (NO + 1);
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const int di = off_comp(DIM, o, 0), dj = DIM == 3 ? off_comp(DIM, o, 1) : 0, dk = off_comp(DIM, o, DIM - 1);
-      const double wo = __ldg(w + o);
-      const double v = wo != 0.0 || o == Traits<DIM>::CENTER ? src[c + di * si + dj * sj + dk] : 0.0;
-      if (o == Traits<DIM>::CENTER) own = v;
-      if (wo != 0.0) As = fma(wo, v, As);
-    }
+  for (int o = 0; o < NO; ++o) {
+    const int di = off_comp(DIM, o, 0), dj = DIM == 3 ? off_comp(DIM, o, 1) : 0, dk = off_comp(DIM, o, DIM - 1);
+    const double v = src[c + di * si + dj * sj + dk];
+    if (o == Traits<DIM>::CENTER) own = v;
+    As = fma(w[o], v, As);
   }
   return As;
 }
 
 template <int DIM>
-__device__ __forceinline__ double cls_invd(const Op<DIM>& op, int cls) {
-  return cls == Traits<DIM>::INTERIOR ? op.invd : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+__device__ __forceinline__ double cls_invd(const double* W, int cls) {
+  return W[cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF];
 }
+
+// copy the level's class table into shared memory (caller syncs)
+// (cp.async: issued before griddepcontrol.wait -- the table is constant -- so its
+// latency overlaps the predecessor kernel; the caller waits with cp.async.wait_all)
+template <int DIM, int NT>
+__device__ __forceinline__ void load_table(double* W, const Op<DIM>& op) {
+  constexpr int T = Traits<DIM>::NCLS * (Traits<DIM>::NOFF + 1);
+  for (int e = threadIdx.x; e < T; e += NT) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(W + e);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(op.tab + e) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void table_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int DIM>
+constexpr int table_doubles() { return Traits<DIM>::NCLS * (Traits<DIM>::NOFF + 1); }
 
 // box origin of this CTA (fine coordinates)
 template <int DIM, int BX>
@@ -143,7 +152,6 @@ template <int DIM, int BX>
 __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc, Op<DIM> op, double omega,
                                                                 const double* __restrict__ b, double* __restrict__ e2,
                                                                 double* __restrict__ bc) {
-  PDL_ENTRY();
   using B = MgBox<DIM, BX>;
   using RS = Reg<DIM, 3, 0, BX>;
   using RE = Reg<DIM, 2, 0, BX>;
@@ -158,8 +166,13 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc,
   double* sb = se1 + RS::SIZE; // |E|
   double* se2 = sb + RE::SIZE; // |E|
   double* sr = se1;            // |R| overlays e1 after phase 2
+  double* W = se2 + RE::SIZE;  // class table
   const int tid = threadIdx.x;
   constexpr int U = 8;
+  load_table<DIM, B::NT>(W, op);
+  PDL_ENTRY();
+  table_wait();
+  __syncthreads();
   // phase 1: e1 on S, b on E (batched loads)
   for (int base = tid; base < RS::SIZE; base += B::NT * U) {
     double bv[U];
@@ -177,7 +190,7 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc,
       int i, j, k;
       S.coords(e, i, j, k);
       const bool in = in_grid<DIM>(g, i, j, k);
-      se1[e] = in ? omega * cls_invd<DIM>(op, class_of<DIM>(g, i, j, k)) * bv[u] : 0.0;
+      se1[e] = in ? omega * cls_invd<DIM>(W, class_of<DIM>(g, i, j, k)) * bv[u] : 0.0;
       if (E.contains(i, j, k)) sb[E.index(i, j, k)] = bv[u];
     }
   }
@@ -190,8 +203,8 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc,
     if (in_grid<DIM>(g, i, j, k)) {
       const int cls = class_of<DIM>(g, i, j, k);
       double own = 0.0;
-      const double As = reg_row<DIM>(op, cls, se1, S, i, j, k, own);
-      v = fma(omega * cls_invd<DIM>(op, cls), sb[e] - As, own);
+      const double As = reg_row<DIM>(W, cls, se1, S, i, j, k, own);
+      v = fma(omega * cls_invd<DIM>(W, cls), sb[e] - As, own);
       const bool inF = i >= fi0 && i < fi0 + B::FI && k >= fk0 && k < fk0 + B::FK &&
                        (DIM == 2 || (j >= fj0 && j < fj0 + B::FJ));
       if (inF) e2[lin_of<DIM>(g, i, j, k)] = v;
@@ -207,7 +220,7 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc,
     if (in_grid<DIM>(g, i, j, k)) {
       const int cls = class_of<DIM>(g, i, j, k);
       double own = 0.0;
-      const double As = reg_row<DIM>(op, cls, se2, E, i, j, k, own);
+      const double As = reg_row<DIM>(W, cls, se2, E, i, j, k, own);
       v = sb[E.index(i, j, k)] - As;
     }
     sr[e] = v;
@@ -241,7 +254,6 @@ template <int DIM, int BX, bool ACC>
 __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, Op<DIM> op, double omega,
                                                               const double* __restrict__ b, const double* __restrict__ e2,
                                                               const double* __restrict__ ec, double* __restrict__ out) {
-  PDL_ENTRY();
   using B = MgBox<DIM, BX>;
   using RP = Reg<DIM, 2, 0, BX>;
   using RQ = Reg<DIM, 1, 0, BX>;
@@ -253,8 +265,11 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, O
   double* sp = sm;
   double* sq = sp + RP::SIZE;
   double* sbq = sq + RQ::SIZE;
+  double* W = sbq + RQ::SIZE;  // class table
   const int tid = threadIdx.x;
   constexpr int U = 8;
+  load_table<DIM, B::NT>(W, op);
+  PDL_ENTRY();
   for (int base = tid; base < RP::SIZE; base += B::NT * U) {
     double ev[U], tv[U];
 #pragma unroll
@@ -287,6 +302,7 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, O
       if (e < RQ::SIZE) sbq[e] = bv[u];
     }
   }
+  table_wait();
   __syncthreads();
   for (int e = tid; e < RQ::SIZE; e += B::NT) {
     int i, j, k;
@@ -295,8 +311,8 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, O
     if (in_grid<DIM>(g, i, j, k)) {
       const int cls = class_of<DIM>(g, i, j, k);
       double own = 0.0;
-      const double As = reg_row<DIM>(op, cls, sp, P, i, j, k, own);
-      v = fma(omega * cls_invd<DIM>(op, cls), sbq[e] - As, own);
+      const double As = reg_row<DIM>(W, cls, sp, P, i, j, k, own);
+      v = fma(omega * cls_invd<DIM>(W, cls), sbq[e] - As, own);
     }
     sq[e] = v;
   }
@@ -307,8 +323,8 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, O
     if (!in_grid<DIM>(g, i, j, k)) continue;
     const int cls = class_of<DIM>(g, i, j, k);
     double own = 0.0;
-    const double As = reg_row<DIM>(op, cls, sq, Q, i, j, k, own);
-    const double x = fma(omega * cls_invd<DIM>(op, cls), sbq[Q.index(i, j, k)] - As, own);
+    const double As = reg_row<DIM>(W, cls, sq, Q, i, j, k, own);
+    const double x = fma(omega * cls_invd<DIM>(W, cls), sbq[Q.index(i, j, k)] - As, own);
     const uint32_t idx = lin_of<DIM>(g, i, j, k);
     if (ACC) out[idx] = out[idx] + x;
     else out[idx] = x;
@@ -325,14 +341,14 @@ inline size_t mg_down_smem() {
   using B = MgBox<DIM, BX>;
   const size_t s = (size_t)(B::FI + 6) * (DIM == 3 ? B::FJ + 6 : 1) * (B::FK + 6);
   const size_t e = (size_t)(B::FI + 4) * (DIM == 3 ? B::FJ + 4 : 1) * (B::FK + 4);
-  return (s + 2 * e) * sizeof(double);
+  return (s + 2 * e + table_doubles<DIM>()) * sizeof(double);
 }
 template <int DIM, int BX>
 inline size_t mg_up_smem() {
   using B = MgBox<DIM, BX>;
   const size_t p = (size_t)(B::FI + 4) * (DIM == 3 ? B::FJ + 4 : 1) * (B::FK + 4);
   const size_t q = (size_t)(B::FI + 2) * (DIM == 3 ? B::FJ + 2 : 1) * (B::FK + 2);
-  return (p + 2 * q) * sizeof(double);
+  return (p + 2 * q + table_doubles<DIM>()) * sizeof(double);
 }
 
 }  // namespace okg
