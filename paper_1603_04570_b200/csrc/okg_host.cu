@@ -542,7 +542,7 @@ static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const
 template <int DIM, int LOAD, int EPI, int TI>
 static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
   static bool attr = false;  // dynamic smem above 48 KB needs an opt-in (per kernel instance)
-  const size_t smem = (size_t)(TI + 2) * TileCfg<DIM>::PSZ * sizeof(double);
+  const size_t smem = tiled_smem_bytes<DIM, LOAD, TI>();
   if (!attr) {
     CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));

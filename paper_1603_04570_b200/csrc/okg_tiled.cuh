@@ -58,6 +58,22 @@ enum TEpi {
   T_CHEB = 5         // Chebyshev step (see k_cheb_step)
 };
 
+// L_PROLONG: the coarse values P e_c needs for a fine tile of TI planes are
+// staged first as a small coarse tile [CI][CJ][CK] (fine tile origin odd or even)
+template <int DIM, int TI>
+struct CoarseTile {
+  static constexpr int CI = TI / 2 + 2;
+  static constexpr int CJ = DIM == 3 ? TileCfg<DIM>::TJ / 2 + 2 : 1;
+  static constexpr int CK = TileCfg<DIM>::TK / 2 + 2;
+  static constexpr int SIZE = CI * CJ * CK;
+};
+
+template <int DIM, int LOAD, int TI>
+constexpr size_t tiled_smem_bytes() {
+  // (TI >= 4 only: on thin tiles the extra pass costs more than the loads it saves)
+  return sizeof(double) * ((size_t)(TI + 2) * TileCfg<DIM>::PSZ + (LOAD == 2 && TI >= 4 ? CoarseTile<DIM, TI>::SIZE : 0));
+}
+
 struct TArgs {
   const double* x;   // staged operand (x, r, d or e)
   const double* b;   // rhs / r_in
@@ -198,8 +214,24 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
     pb[t] = (EpiNeeds<EPI>::B && ok) ? a.b[idx] : 0.0;
     pp[t] = (EpiNeeds<EPI>::P2 && ok) ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx]) : 0.0;
   }
+  // L_PROLONG: coarse tile covering the fine planes/rows/columns of the staged tile
+  using CT = CoarseTile<DIM, TI>;
+  double* ct = tile + (TI + 2) * TC::PSZ;
+  const int cbi = (i0 - 1) >> 1, cbj = DIM == 3 ? (j0 - 1) >> 1 : 0, cbk = (k0 - 1) >> 1;
+  constexpr bool CSTAGE = LOAD == L_PROLONG && TI >= 4;
+  if (CSTAGE) {
+    for (int e = tid; e < CT::SIZE; e += TC::NT) {
+      const int ck = e % CT::CK, t = e / CT::CK;
+      const int cj = DIM == 3 ? t % CT::CJ : 0, ci = DIM == 3 ? t / CT::CJ : t;
+      const int gi = cbi + ci, gj = cbj + cj, gk = cbk + ck;
+      const bool in = gi <= a.gc.n && gk <= a.gc.n && (DIM == 2 || gj <= a.gc.n);
+      const uint32_t lin = DIM == 3 ? (uint32_t)gi * a.gc.ps + (uint32_t)gj * a.gc.s + gk : (uint32_t)gi * a.gc.s + gk;
+      ct[e] = in ? __ldg(a.x2 + lin) : 0.0;
+    }
+  }
   // stage planes i0-1 .. i0+ni (linear order, 8 loads in flight per thread per batch;
   // the best of the variants measured by tools/stencil_bench.cu)
+  constexpr int LOAD_STAGE = CSTAGE ? L_PLAIN : LOAD;
   const int total = (ni + 2) * TC::PSZ;
   constexpr int U = 8;
   for (int base = tid; base < total; base += TC::NT * U) {
@@ -218,7 +250,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
         const int ip = i0 - 1 + p;
         if (gk <= g.n && gj <= g.n) {
           const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
-          v[u] = stage_val<DIM, LOAD>(g, op, a, lin, ip, gj, gk);
+          v[u] = stage_val<DIM, LOAD_STAGE>(g, op, a, lin, ip, gj, gk);
         }
       }
     }
@@ -229,6 +261,26 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
     }
   }
   __syncthreads();
+  if (CSTAGE) {
+    // staged value e + P e_c (x + t, as prolong_at / k_prolong_add: multigrid.hpp:111-112)
+    constexpr int CSI = CT::CJ * CT::CK, CSJ = CT::CK;
+    for (int e = tid; e < total; e += TC::NT) {
+      const int p = e / TC::PSZ;
+      const int r = e - p * TC::PSZ;
+      const int hj = DIM == 3 ? r / TC::PW : 0;
+      const int hk = DIM == 3 ? r - hj * TC::PW : r;
+      const int gj = DIM == 3 ? j0 - 1 + hj : 0;
+      const int gk = k0 - 1 + hk;
+      const int ip = i0 - 1 + p;
+      if (gk > g.n || gj > g.n) continue;
+      const int li = (ip >> 1) - cbi, lj = DIM == 3 ? (gj >> 1) - cbj : 0, lk = (gk >> 1) - cbk;
+      const int hi = ((ip + 1) >> 1) - cbi, hj2 = DIM == 3 ? ((gj + 1) >> 1) - cbj : 0, hk2 = ((gk + 1) >> 1) - cbk;
+      const int lo = li * CSI + lj * CSJ + lk, up = hi * CSI + hj2 * CSJ + hk2;
+      const double t = lo == up ? ct[lo] : fma(0.5, ct[up], 0.5 * ct[lo]);
+      tile[e] = tile[e] + t;
+    }
+    __syncthreads();
+  }
   if (!active) return;
   // all TI vertex chains are computed unconditionally (no branch between them, so
   // their dependent FMA chains interleave); only the stores are predicated
