@@ -70,7 +70,7 @@ typedef struct okg_params {
   int32_t mg_fuse;          /* temporally blocked V(2,2) level kernels (one "down" and one
                                "up" launch per level): 0 = default (2D: every level
                                but the finest; 3D: levels with n <= 32), 1 = every
-                               level, < 0 = never */
+                               level, 2 = every level but the finest, < 0 = never */
   int32_t nslabs;           /* slab decomposition: split the mesh into this
                                many x-plane slabs, one host thread + CUDA stream each;
                                0/1 = one slab.  Results equal the one-slab solve up to
@@ -92,6 +92,8 @@ typedef struct okg_step_stats {
   double seconds;                      /* wall time of newton_solve       */
   int32_t converged;
   int64_t kernel_launches;             /* kernels (incl. graph nodes) launched */
+  double mass;                         /* b^T u at the new level (okg_advance) */
+  double energy;                       /* energy of the new level (okg_advance with_energy; else NaN) */
 } okg_step_stats;
 
 /* ---- okflow::KrylovResult (krylov.hpp:21-28) --------------------------------- */
@@ -193,6 +195,23 @@ int okg_newton_step(okg_ctx* ctx, okg_step_stats* stats);
 /* same, through host buffers: H2D of (u_old, w_old), solve, D2H of (u, w) */
 int okg_newton_step_host(okg_ctx* ctx, const double* u_old, const double* w_old,
                          double* u_new, double* w_new, okg_step_stats* stats);
+
+/* ---- diagnostics and initial state -------------------------------
+ * u: host array of N doubles, or NULL for the context's current state */
+/* total_mass = b^T u (model.hpp:46-48) */
+int okg_total_mass(okg_ctx* ctx, const double* u, double* mass);
+/* integrate_double_well (assembly.hpp:220-245), closed form of the degree-4 integral */
+int okg_double_well(okg_ctx* ctx, const double* u, double* value);
+/* energy (model.hpp:56-86): grad + double well + nonlocal term via Jacobi CG on K
+ * with the constant nullspace projected out (rtol 1e-10, 2000 iterations);
+ * OKG_EINCONSISTENT when the potential rhs is not mean-zero, OKG_ENUMERICAL when
+ * the CG does not converge -- exactly the reference's failure modes */
+int okg_energy(okg_ctx* ctx, const double* u, double* energy, int32_t* cg_iters);
+/* initial_state (model.hpp:93-114): the context's state becomes u0 (cosine bump),
+ * w0 (Jacobi CG mass solve, rtol 1e-12), t = 0, step = 0 */
+int okg_initial_state(okg_ctx* ctx, int32_t* cg_iters);
+/* advance (model.hpp:218-227): okg_newton_step + mass (+ energy) of the new state */
+int okg_advance(okg_ctx* ctx, int32_t with_energy, okg_step_stats* stats);
 
 /* ---- per-operator entry points on HOST pointers (any nslabs) ---------------------
  * Same operations as the device-pointer entry points below; the context scatters

@@ -335,15 +335,102 @@ inline std::pair<State, IterationStats> newton_solve(const State& old, SchurCont
   return {std::move(next), std::move(s)};
 }
 
+inline IterationStats from_stats(const okg_step_stats& st) {
+  IterationStats s;
+  s.step = st.step;
+  s.t = st.t;
+  s.newton_iters = st.newton_iters;
+  for (int i = 0; i < st.newton_iters && i < OKG_MAX_NEWTON; ++i) s.gmres_iters.push_back(st.gmres_iters[i]);
+  s.residual_norm = st.residual_norm;
+  s.seconds = st.seconds;
+  s.converged = st.converged != 0;
+  s.mass = st.mass;
+  s.energy = st.energy;
+  return s;
+}
+
+// ---- model.hpp:46-114: diagnostics and initial state on the device -------------------------
+inline double total_mass(const SchurContext& ctx, const Vector& u) {  // b^T u
+  double m = 0.0;
+  check(okg_total_mass(ctx.handle(), u.data(), &m));
+  return m;
+}
+inline double integrate_double_well(const SchurContext& ctx, const Vector& u) {
+  double v = 0.0;
+  check(okg_double_well(ctx.handle(), u.data(), &v));
+  return v;
+}
+inline double energy(const SchurContext& ctx, const Vector& u, const SolverConfig& /*cfg: ctx holds it*/) {
+  if (static_cast<long>(u.size()) != ctx.rows()) throw std::invalid_argument("energy: vector length mismatch");
+  double e = 0.0;
+  check(okg_energy(ctx.handle(), u.data(), &e, nullptr));
+  return e;
+}
+inline State initial_state(SchurContext& ctx, const SolverConfig& /*cfg*/) {
+  check(okg_initial_state(ctx.handle(), nullptr));
+  State s;
+  s.u.resize(static_cast<size_t>(ctx.rows()));
+  s.w.resize(s.u.size());
+  check(okg_get_state(ctx.handle(), s.u.data(), s.w.data(), &s.t, &s.step));
+  return s;
+}
+
+// advance (model.hpp:218-227): newton_solve + mass + energy of the new state
 inline std::pair<State, IterationStats> advance(const State& state, SchurContext& ctx, const SolverConfig& cfg) {
-  auto res = newton_solve(state, ctx, cfg);
-  // total_mass = b^T u with b = M 1 (model.hpp:46-48)
-  const Vector ones(static_cast<size_t>(ctx.rows()), 1.0);
-  const Vector b = ctx.apply(OKG_OP_M, ones, ones.size());
-  double mass = 0.0;
-  for (size_t i = 0; i < b.size(); ++i) mass += b[i] * res.first.u[i];
-  res.second.mass = mass;
-  return res;
+  const size_t n = static_cast<size_t>(ctx.rows());
+  if (state.u.size() != n || state.w.size() != n) throw std::invalid_argument("residual: states do not match the mesh");
+  (void)cfg;
+  check(okg_set_state(ctx.handle(), state.u.data(), state.w.data(), state.t, state.step));
+  okg_step_stats st;
+  check(okg_advance(ctx.handle(), 1, &st));
+  State next;
+  next.u.resize(n);
+  next.w.resize(n);
+  check(okg_get_state(ctx.handle(), next.u.data(), next.w.data(), &next.t, &next.step));
+  return {std::move(next), from_stats(st)};
+}
+
+// run_simulation (model.hpp:243-279), device-resident between steps; the state is
+// copied to the host only for the on_state observer
+struct SimulationResult {
+  std::vector<IterationStats> stats;
+  State final_state;
+};
+
+inline SimulationResult run_simulation(const SolverConfig& cfg, const std::function<void(const State&)>& on_state = {},
+                                       double shat_perturb = 0.0,
+                                       const std::function<void(const IterationStats&)>& on_stats = {}) {
+  cfg.validate();
+  SchurContext ctx = make_schur_context(cfg, shat_perturb);
+  SimulationResult result;
+  State state = initial_state(ctx, cfg);
+  IterationStats init;
+  init.mass = total_mass(ctx, state.u);
+  init.energy = energy(ctx, state.u, cfg);
+  result.stats.push_back(init);
+  if (on_stats) on_stats(init);
+  if (on_state) on_state(state);
+  for (int k = 0; k < cfg.n_steps; ++k) {
+    okg_step_stats st;
+    check(okg_advance(ctx.handle(), 1, &st));
+    const IterationStats s = from_stats(st);
+    result.stats.push_back(s);
+    if (on_stats) on_stats(s);
+    if (!s.converged)
+      throw NumericalError("run_simulation: nonlinear solve failed at step " + std::to_string(s.step) +
+                           " (residual " + std::to_string(s.residual_norm) + ")");
+    if (on_state) {
+      state.u.resize(static_cast<size_t>(ctx.rows()));
+      state.w.resize(state.u.size());
+      check(okg_get_state(ctx.handle(), state.u.data(), state.w.data(), &state.t, &state.step));
+      on_state(state);
+    }
+  }
+  result.final_state.u.resize(static_cast<size_t>(ctx.rows()));
+  result.final_state.w.resize(result.final_state.u.size());
+  check(okg_get_state(ctx.handle(), result.final_state.u.data(), result.final_state.w.data(), &result.final_state.t,
+                      &result.final_state.step));
+  return result;
 }
 
 }  // namespace okg

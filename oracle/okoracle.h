@@ -112,6 +112,17 @@ int oko_newton_solve(void* ctx, const double* u_old, const double* w_old,
 /* Lanczos bounds on diag(M)^-1 M (krylov.hpp:296-320), standalone */
 int oko_jacobi_spectrum(void* ctx, double* lo, double* hi);
 
+/* ---- diagnostics and initial state ---- */
+/* total_mass = b^T u (model.hpp:46-48) */
+int oko_total_mass(void* ctx, const double* u, double* mass);
+/* integrate_double_well (assembly.hpp:220-245), degree-4 rule, Kahan sum */
+int oko_double_well(void* ctx, const double* u, double* value);
+/* energy (model.hpp:56-86); cg_iters = iterations of the potential solve
+ * (-1 when the implementation does not report them, 0 when sigma == 0) */
+int oko_energy(void* ctx, const double* u, double* energy, int* cg_iters);
+/* initial_state (model.hpp:93-114): u0 (cosine bump), w0 (mass solve) */
+int oko_initial_state(void* ctx, double* u, double* w, int* cg_iters);
+
 /* builder-defined seeded IC, SURVEY.md section 8(d) (counter-based splitmix64) */
 void oko_seeded_ic(long nverts, unsigned long long seed, double m, double* u);
 

@@ -1597,3 +1597,177 @@ void oko_seeded_ic(long nverts, unsigned long long seed, double m, double* u) {
     u[g] = m + 0.01 * U;
   }
 }
+
+/* ---- diagnostics and initial state -------------------------- */
+
+/* conjugate_gradient (krylov.hpp:424-479) with the Jacobi preconditioner of
+ * make_jacobi_preconditioner (operator.hpp:53-64: z = r / diag) and an optional
+ * unit-norm nullspace vector ns (project: v -= (v . ns) ns) */
+static int conjugate_gradient(const csr* A, const double* diag, const double* b, double rel_tol, int max_iter,
+                              const double* ns, double* x, int* iters, int* converged) {
+  const long n = A->nr;
+  if (!all_finite(b, n)) FAIL(OKO_EINVAL, "cg rhs: vector contains NaN/Inf");
+  double* r = dcopy(b, n);
+  double* z = dalloc(n);
+  double* p = dalloc(n);
+  double* Ap = dalloc(n);
+  memset(x, 0, (size_t)n * sizeof(double));
+  *iters = 0;
+  *converged = 0;
+#define PROJECT(v)                            \
+  do {                                        \
+    if (ns) axpy(-dot(v, ns, n), ns, v, n);   \
+  } while (0)
+  PROJECT(r);
+  const double norm_b = norm2(r, n);
+  int st = OKO_OK;
+  if (norm_b == 0.0) {
+    *converged = 1;
+  } else {
+    const double target = rel_tol * norm_b;
+    for (long i = 0; i < n; ++i) z[i] = r[i] / diag[i];
+    PROJECT(z);
+    memcpy(p, z, (size_t)n * sizeof(double));
+    double rz = dot(r, z, n);
+    for (int it = 0; it < max_iter; ++it) {
+      spmv(A, p, Ap);
+      const double pAp = dot(p, Ap, n);
+      if (pAp <= 0.0) {
+        snprintf(g_err, sizeof g_err, "cg: operator not positive definite on iterate");
+        st = OKO_ENUMERICAL;
+        break;
+      }
+      const double alpha = rz / pAp;
+      axpy(alpha, p, x, n);
+      axpy(-alpha, Ap, r, n);
+      PROJECT(r);
+      ++*iters;
+      const double rn = norm2(r, n);
+      if (rn <= target) {
+        *converged = 1;
+        break;
+      }
+      for (long i = 0; i < n; ++i) z[i] = r[i] / diag[i];
+      PROJECT(z);
+      const double rz_new = dot(r, z, n);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (long i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    }
+  }
+#undef PROJECT
+  free(r);
+  free(z);
+  free(p);
+  free(Ap);
+  return st;
+}
+
+/* integrate_double_well (assembly.hpp:220-245): degree-4 rule, Kahan-compensated cell sum */
+static double integrate_double_well(const mesh_t* m, const double* u) {
+  quadrule_t q;
+  simplex_quadrature(m->dim, 4, &q);
+  const int vpc = m->dim + 1;
+  const double ref_measure = m->dim == 2 ? 0.5 : 1.0 / 6.0;
+  double total = 0.0, comp = 0.0;
+  for (long c = 0; c < m->ncell; ++c) {
+    const int* cv = m->cells + c * vpc;
+    const double scale = cell_volume(m, c) / ref_measure;
+    double cell = 0.0;
+    for (int p = 0; p < q.np; ++p) {
+      const double* bq = q.pts + p * vpc;
+      double uq = 0.0;
+      for (int k = 0; k < vpc; ++k) uq += u[cv[k]] * bq[k];
+      const double w = 1.0 - uq * uq;
+      cell += q.w[p] * w * w;
+    }
+    const double y = cell * scale - comp;
+    const double t = total + y;
+    comp = (t - total) - y;
+    total = t;
+  }
+  return total;
+}
+
+int oko_total_mass(void* ctx, const double* u, double* mass) {
+  port_ctx* c = (port_ctx*)ctx;
+  *mass = dot(c->b, u, c->mesh.nv); /* model.hpp:46-48 */
+  return OKO_OK;
+}
+
+int oko_double_well(void* ctx, const double* u, double* value) {
+  *value = integrate_double_well(&((port_ctx*)ctx)->mesh, u);
+  return OKO_OK;
+}
+
+/* energy (model.hpp:56-86) */
+int oko_energy(void* ctx, const double* u, double* e, int* cg_iters) {
+  port_ctx* c = (port_ctx*)ctx;
+  const long n = c->mesh.nv;
+  const double eps = c->p.eps, sigma = c->p.sigma, mm = c->p.m;
+  double* Ku = dalloc(n);
+  spmv(&c->K, u, Ku);
+  const double grad_term = 0.5 * eps * eps * dot(u, Ku, n);
+  free(Ku);
+  const double well_term = 0.25 * integrate_double_well(&c->mesh, u);
+  double nonlocal = 0.0;
+  if (cg_iters) *cg_iters = 0;
+  if (sigma != 0.0) {
+    double* rhs = dalloc(n);
+    spmv(&c->M, u, rhs);
+    axpy(-mm, c->b, rhs, n);
+    double mean = 0.0;
+    for (long i = 0; i < n; ++i) mean += rhs[i];
+    if (fabs(mean) > 1e-6) {
+      free(rhs);
+      FAIL(OKO_EINCONSISTENT, "energy: potential right-hand side is not mean-zero (|sum| = %f)", fabs(mean));
+    }
+    double* ones = dalloc(n);
+    for (long i = 0; i < n; ++i) ones[i] = 1.0 / sqrt((double)n);
+    double* diag = dalloc(n);
+    csr_diag(&c->K, diag);
+    double* phi = dalloc(n);
+    int its = 0, conv = 0;
+    const int st = conjugate_gradient(&c->K, diag, rhs, 1e-10, 2000, ones, phi, &its, &conv);
+    if (cg_iters) *cg_iters = its;
+    if (st == OKO_OK && conv) nonlocal = 0.5 * sigma * dot(phi, rhs, n);
+    free(ones);
+    free(diag);
+    free(phi);
+    free(rhs);
+    if (st != OKO_OK) return st;
+    if (!conv) FAIL(OKO_ENUMERICAL, "energy: potential solve did not converge");
+  }
+  *e = grad_term + well_term + nonlocal;
+  return OKO_OK;
+}
+
+/* initial_state (model.hpp:93-114) */
+int oko_initial_state(void* ctx, double* u, double* w, int* cg_iters) {
+  port_ctx* c = (port_ctx*)ctx;
+  const mesh_t* m = &c->mesh;
+  const long n = m->nv;
+  const double kPi = 3.14159265358979323846;
+  for (long v = 0; v < n; ++v) {
+    const double x = m->vert[v * m->dim], y = m->vert[v * m->dim + 1];
+    const double z = m->dim == 3 ? m->vert[v * m->dim + 2] : 0.0;
+    u[v] = c->p.m + cos(2.0 * kPi * x) * cos(2.0 * kPi * y) * cos(2.0 * kPi * z) / 50.0;
+  }
+  double* rhs = dalloc(n);
+  spmv(&c->K, u, rhs);
+  scal(c->p.eps * c->p.eps, rhs, n);
+  double* nl = dalloc(n);
+  assemble_nonlinear(m, u, nl);
+  axpy(1.0, nl, rhs, n);
+  free(nl);
+  double* diag = dalloc(n);
+  csr_diag(&c->M, diag);
+  int its = 0, conv = 0;
+  const int st = conjugate_gradient(&c->M, diag, rhs, 1e-12, 1000, NULL, w, &its, &conv);
+  if (cg_iters) *cg_iters = its;
+  free(diag);
+  free(rhs);
+  if (st != OKO_OK) return st;
+  if (!conv) FAIL(OKO_ENUMERICAL, "initial_state: mass solve did not converge");
+  return OKO_OK;
+}

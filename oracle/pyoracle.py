@@ -91,6 +91,10 @@ def load(kind: str = "ref"):
     lib.oko_jacobi_spectrum.argtypes = [C.c_void_p, _dp, _dp]
     lib.oko_seeded_ic.argtypes = [C.c_long, C.c_ulonglong, C.c_double, _dp]
     lib.oko_default_params.argtypes = [C.POINTER(Params)]
+    lib.oko_total_mass.argtypes = [C.c_void_p, _dp, _dp]
+    lib.oko_double_well.argtypes = [C.c_void_p, _dp, _dp]
+    lib.oko_energy.argtypes = [C.c_void_p, _dp, _dp, _ip]
+    lib.oko_initial_state.argtypes = [C.c_void_p, _dp, _dp, _ip]
     _loaded[kind] = lib
     return lib
 
@@ -258,3 +262,29 @@ class Oracle:
         lo, hi = C.c_double(), C.c_double()
         _check(self.lib, self.lib.oko_jacobi_spectrum(self.h, C.byref(lo), C.byref(hi)))
         return lo.value, hi.value
+
+    # ---- diagnostics and initial state ----
+    def total_mass(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = C.c_double()
+        _check(self.lib, self.lib.oko_total_mass(self.h, _p(u), C.byref(out)))
+        return out.value
+
+    def double_well(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = C.c_double()
+        _check(self.lib, self.lib.oko_double_well(self.h, _p(u), C.byref(out)))
+        return out.value
+
+    def energy(self, u):
+        """-> (energy, cg_iters); cg_iters is -1 for the compiled reference (not exposed)."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out, it = C.c_double(), C.c_int()
+        _check(self.lib, self.lib.oko_energy(self.h, _p(u), C.byref(out), C.byref(it)))
+        return out.value, it.value
+
+    def initial_state(self):
+        u, w = np.empty(self.n), np.empty(self.n)
+        it = C.c_int()
+        _check(self.lib, self.lib.oko_initial_state(self.h, _p(u), _p(w), C.byref(it)))
+        return u, w, it.value

@@ -350,4 +350,36 @@ void oko_seeded_ic(long nverts, unsigned long long seed, double m, double* u) {
   }
 }
 
+int oko_total_mass(void* ctx, const double* u, double* mass) {
+  return guarded([&] {
+    auto* c = static_cast<RefCtx*>(ctx);
+    *mass = total_mass(c->ops, vec_in(u, c->mesh.num_vertices()));
+  });
+}
+
+int oko_double_well(void* ctx, const double* u, double* value) {
+  return guarded([&] {
+    auto* c = static_cast<RefCtx*>(ctx);
+    *value = integrate_double_well(c->mesh, vec_in(u, c->mesh.num_vertices()));
+  });
+}
+
+int oko_energy(void* ctx, const double* u, double* e, int* cg_iters) {
+  return guarded([&] {
+    auto* c = static_cast<RefCtx*>(ctx);
+    *e = energy(c->mesh, c->ops, vec_in(u, c->mesh.num_vertices()), c->cfg);
+    if (cg_iters) *cg_iters = -1;  // not exposed by the reference
+  });
+}
+
+int oko_initial_state(void* ctx, double* u, double* w, int* cg_iters) {
+  return guarded([&] {
+    auto* c = static_cast<RefCtx*>(ctx);
+    const State s = initial_state(c->mesh, c->ops, c->cfg);
+    vec_out(s.u, u);
+    vec_out(s.w, w);
+    if (cg_iters) *cg_iters = -1;
+  });
+}
+
 }  // extern "C"

@@ -30,7 +30,8 @@ __all__ = [
     "SolverConfig", "StructuredMesh", "build_mesh", "State", "IterationStats", "KrylovResult",
     "SchurContext", "make_schur_context", "compute_c", "residual", "newton_solve", "advance",
     "run_steps", "apply_block", "jacobian_operator", "block_preconditioner", "LinearOperator",
-    "gmres", "seeded_ic", "DeviceArray", "total_mass",
+    "gmres", "seeded_ic", "DeviceArray", "total_mass", "energy", "integrate_double_well",
+    "initial_state", "run_simulation", "SimulationResult",
     "InvalidArgument", "NumericalError", "ConfigError", "InconsistentState", "CannotCoarsen",
     "CudaError", "OkgError",
 ]
@@ -200,7 +201,7 @@ class IterationStats:
     gmres_iters: List[int] = field(default_factory=list)
     residual_norm: float = 0.0
     mass: float = 0.0
-    energy: float = float("nan")  # energy() is out of scope for the GPU path
+    energy: float = float("nan")  # filled by advance / run_simulation (okg_energy)
     seconds: float = 0.0
     converged: bool = True
     kernel_launches: int = 0
@@ -396,13 +397,54 @@ class SchurContext:
         check(lib.okg_newton_step(self.handle, C.byref(ss)))
         return _stats(ss)
 
+    def advance_resident(self, with_energy: bool = True) -> IterationStats:
+        """advance (model.hpp:218-227): newton_solve + mass (+ energy) of the new state."""
+        ss = _lib.StepStats()
+        check(lib.okg_advance(self.handle, 1 if with_energy else 0, C.byref(ss)))
+        return _stats(ss)
+
+    # ---- diagnostics (model.hpp:46-114); u=None: the device-resident state ----
+    def _u_arg(self, u):
+        if u is None:
+            return None, None
+        a = np.ascontiguousarray(u, dtype=np.float64)
+        if a.size != self.n:
+            raise InvalidArgument("energy: vector length mismatch")
+        return a, a.ctypes.data_as(_lib._dp)
+
+    def total_mass(self, u: Optional[np.ndarray] = None) -> float:
+        keep, p = self._u_arg(u)
+        out = C.c_double()
+        check(lib.okg_total_mass(self.handle, p, C.byref(out)))
+        return out.value
+
+    def double_well(self, u: Optional[np.ndarray] = None) -> float:
+        keep, p = self._u_arg(u)
+        out = C.c_double()
+        check(lib.okg_double_well(self.handle, p, C.byref(out)))
+        return out.value
+
+    def energy(self, u: Optional[np.ndarray] = None) -> Tuple[float, int]:
+        """-> (energy, CG iterations of the potential solve)."""
+        keep, p = self._u_arg(u)
+        out, it = C.c_double(), C.c_int32()
+        check(lib.okg_energy(self.handle, p, C.byref(out), C.byref(it)))
+        return out.value, it.value
+
+    def initial_state(self) -> Tuple[State, int]:
+        """initial_state (model.hpp:93-114) into the context; -> (state, CG iterations)."""
+        it = C.c_int32()
+        check(lib.okg_initial_state(self.handle, C.byref(it)))
+        return self.get_state(), it.value
+
 
 def _stats(ss: "_lib.StepStats") -> IterationStats:
     ni = ss.newton_iters
     return IterationStats(step=ss.step, t=ss.t, newton_iters=ni,
                           gmres_iters=[int(ss.gmres_iters[i]) for i in range(min(ni, _lib.OKG_MAX_NEWTON))],
                           residual_norm=ss.residual_norm, seconds=ss.seconds,
-                          converged=bool(ss.converged), kernel_launches=int(ss.kernel_launches))
+                          converged=bool(ss.converged), kernel_launches=int(ss.kernel_launches),
+                          mass=float(ss.mass), energy=float(ss.energy))
 
 
 def make_schur_context(mesh: StructuredMesh, cfg: SolverConfig, shat_perturb: float = 0.0,
@@ -477,17 +519,76 @@ def newton_solve(old: State, mesh: StructuredMesh, ctx: SchurContext,
 
 
 def total_mass(mesh: StructuredMesh, ctx: SchurContext, u: np.ndarray) -> float:
-    """model.hpp:46-48: b^T u, with b = M 1 (row sums of M are the loads, assembly.hpp:130)."""
-    b = ctx.apply(_lib.OP_M, np.ones(ctx.n))
-    return float(np.dot(b, u))
+    """model.hpp:46-48: b^T u (okg_total_mass)."""
+    return ctx.total_mass(u)
+
+
+def integrate_double_well(mesh: StructuredMesh, ctx: SchurContext, u: np.ndarray) -> float:
+    """assembly.hpp:220-245 (okg_double_well)."""
+    return ctx.double_well(u)
+
+
+def energy(mesh: StructuredMesh, ctx: SchurContext, u: np.ndarray, cfg: Optional[SolverConfig] = None) -> float:
+    """model.hpp:56-86 (okg_energy): raises InconsistentState / NumericalError like the reference."""
+    if len(u) != mesh.num_vertices():
+        raise InvalidArgument("energy: vector length mismatch")
+    return ctx.energy(u)[0]
+
+
+def initial_state(mesh: StructuredMesh, ctx: SchurContext, cfg: Optional[SolverConfig] = None) -> State:
+    """model.hpp:93-114 (okg_initial_state)."""
+    return ctx.initial_state()[0]
 
 
 def advance(state: State, mesh: StructuredMesh, ctx: SchurContext,
             cfg: Optional[SolverConfig] = None) -> Tuple[State, IterationStats]:
-    """model.hpp:218-227 minus the energy diagnostic (out of scope)."""
-    nxt, stats = newton_solve(state, mesh, ctx, cfg)
-    stats.mass = total_mass(mesh, ctx, nxt.u)
-    return nxt, stats
+    """model.hpp:218-227: newton_solve + mass + energy of the new state."""
+    if len(state.u) != mesh.num_vertices():
+        raise InvalidArgument("residual: states do not match the mesh")
+    ctx.set_state(state)
+    stats = ctx.advance_resident(True)
+    return ctx.get_state(), stats
+
+
+@dataclass
+class SimulationResult:
+    mesh: StructuredMesh
+    stats: List[IterationStats]
+    final_state: State
+
+
+def run_simulation(cfg: SolverConfig, on_state: Optional[Callable[[StructuredMesh, State], None]] = None,
+                   shat_perturb: float = 0.0, on_stats: Optional[Callable[[IterationStats], None]] = None,
+                   ctx: Optional[SchurContext] = None, with_energy: bool = True) -> SimulationResult:
+    """run_simulation (model.hpp:243-279): initial_state, then cfg.n_steps advances, all
+    device-resident; the state leaves the GPU only for `on_state` observers."""
+    cfg.validate()
+    mesh = build_mesh(cfg.dim, cfg.n, with_arrays=False)
+    own = ctx is None
+    if own:
+        ctx = make_schur_context(mesh, cfg, shat_perturb)
+    try:
+        state, _ = ctx.initial_state()
+        init = IterationStats(step=0, t=0.0, mass=ctx.total_mass(), energy=ctx.energy()[0] if with_energy else float("nan"))
+        stats = [init]
+        if on_stats:
+            on_stats(init)
+        if on_state:
+            on_state(mesh, state)
+        for _ in range(cfg.n_steps):
+            st = ctx.advance_resident(with_energy)
+            stats.append(st)
+            if on_stats:
+                on_stats(st)
+            if not st.converged:
+                raise NumericalError(f"run_simulation: nonlinear solve failed at step {st.step} "
+                                     f"(residual {st.residual_norm})")
+            if on_state:
+                on_state(mesh, ctx.get_state())
+        return SimulationResult(mesh, stats, ctx.get_state())
+    finally:
+        if own:
+            ctx.close()
 
 
 def run_steps(ctx: SchurContext, state: State, n_steps: int,

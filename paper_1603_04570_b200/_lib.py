@@ -54,6 +54,7 @@ class StepStats(C.Structure):
         ("step", C.c_int32), ("t", C.c_double), ("newton_iters", C.c_int32),
         ("gmres_iters", C.c_int32 * OKG_MAX_NEWTON), ("residual_norm", C.c_double),
         ("seconds", C.c_double), ("converged", C.c_int32), ("kernel_launches", C.c_int64),
+        ("mass", C.c_double), ("energy", C.c_double),
     ]
 
 
@@ -146,6 +147,11 @@ _SIGS = {
     "okg_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "okg_slab_stream": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp)]),
     "okg_nccl_unique_id": (C.c_int, [_vp, C.c_size_t]),
+    "okg_total_mass": (C.c_int, [_vp, _dp, _dp]),
+    "okg_double_well": (C.c_int, [_vp, _dp, _dp]),
+    "okg_energy": (C.c_int, [_vp, _dp, _dp, C.POINTER(C.c_int32)]),
+    "okg_initial_state": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
+    "okg_advance": (C.c_int, [_vp, C.c_int32, C.POINTER(StepStats)]),
     "okg_create_rank": (C.c_int, [C.POINTER(Params), C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
     "okg_slab_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),

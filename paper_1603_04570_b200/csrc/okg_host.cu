@@ -33,6 +33,7 @@
 
 #include "../../include/okg.h"
 #include "okg_kernels.cuh"
+#include "okg_diag.cuh"
 #include "okg_nccl.h"
 #include "okg_tables.h"
 
@@ -1347,6 +1348,155 @@ static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
   hi = 1.1 * ev.back();
 }
 
+// ---- diagnostics and initial state (okg_diag.cuh) -------------------------
+// dot of two level-0 vectors over the owned vertices, allreduced over the slabs
+static double dotv(okg_ctx* c, const double* a, const double* b) {
+  const size_t ne = c->seg.len;
+  const Seg s1{c->seg.off, ne, c->B};
+  launch(c, k_dot, vblk(ne), BS, 0, (const double*)F(c, a), (const double*)F(c, b), s1, ne, red(c, R_DOT));
+  note(c);
+  sync_read(c, R_DOT, 1);
+  allreduce(c, R_DOT, 1);
+  return c->hred[R_DOT];
+}
+
+// conjugate_gradient (krylov.hpp:424-479) with the Jacobi preconditioner of A
+// (operator.hpp:53-64) and an optional unit nullspace vector ns; b, x, ns are
+// level-0 vectors; returns the iteration count
+template <int DIM>
+static int cg(okg_ctx* c, const HostOp& A, const double* b, double* x, double rel_tol, int max_iter,
+              const double* ns, bool& converged) {
+  const size_t B = c->B;
+  double *r = c->cd0, *z = c->cd1, *p = c->cr, *Ap = c->st;
+  auto project = [&](double* v) {
+    if (ns) axpy(c, -dotv(c, v, ns), F(c, ns), F(c, v), B);
+  };
+  converged = false;
+  CK(cudaMemsetAsync(F(c, x), 0, B * sizeof(double), c->stream));
+  copy(c, F(c, b), F(c, r), B);
+  {  // require_finite(b, "cg rhs") (krylov.hpp:429): a non-finite entry makes ||b|| non-finite
+    const double bb = dotv(c, b, b);
+    if (!std::isfinite(bb)) THROW(OKG_EINVAL, "cg rhs: vector contains NaN/Inf");
+  }
+  project(r);
+  const double norm_b = std::sqrt(dotv(c, r, r));
+  if (norm_b == 0.0) {
+    converged = true;
+    return 0;
+  }
+  const double target = rel_tol * norm_b;
+  const Op<DIM> op = dev_op<DIM>(A);
+  launch(c, k_divdiag<DIM>, own(c->fine), BS, 0, c->fine, op, (const double*)r, z);
+  note(c);
+  project(z);
+  copy(c, F(c, z), F(c, p), B);
+  double rz = dotv(c, r, z);
+  int it = 0;
+  for (; it < max_iter;) {
+    apply_level<DIM>(c, 0, A, p, Ap);
+    const double pAp = dotv(c, p, Ap);
+    if (pAp <= 0.0) THROW(OKG_ENUMERICAL, "cg: operator not positive definite on iterate");
+    const double alpha = rz / pAp;
+    axpy(c, alpha, F(c, p), F(c, x), B);
+    axpy(c, -alpha, F(c, Ap), F(c, r), B);
+    project(r);
+    ++it;
+    const double rn = std::sqrt(dotv(c, r, r));
+    if (rn <= target) {
+      converged = true;
+      break;
+    }
+    launch(c, k_divdiag<DIM>, own(c->fine), BS, 0, c->fine, op, (const double*)r, z);
+    note(c);
+    project(z);
+    const double rz_new = dotv(c, r, z);
+    const double beta = rz_new / rz;
+    rz = rz_new;
+    launch(c, k_xpby, vblk(B), BS, 0, (const double*)F(c, z), beta, F(c, p), B);
+    note(c);
+  }
+  return it;
+}
+
+// total_mass = b^T u (model.hpp:46-48)
+template <int DIM>
+static double total_mass_impl(okg_ctx* c, const double* u) {
+  launch(c, k_mass<DIM>, vblk(c->fine.hi - c->fine.lo), BS, 0, c->fine, (const double*)c->b_tab, u, red(c, R_DOT));
+  note(c);
+  sync_read(c, R_DOT, 1);
+  allreduce(c, R_DOT, 1);
+  return c->hred[R_DOT];
+}
+
+// integrate_double_well (assembly.hpp:220-245)
+template <int DIM>
+static double double_well_impl(okg_ctx* c, const double* u) {
+  exchange(c, 0, u);
+  const Grid& g = c->fine;
+  const size_t cells = (size_t)std::max(0, std::min(g.ihi, g.n) - g.ilo) * (DIM == 3 ? (size_t)g.n * g.n : g.n);
+  const double vol = DIM == 2 ? c->h * c->h / 2.0 : c->h * c->h * c->h / 6.0;
+  launch(c, k_double_well<DIM>, vblk(cells), BS, 0, g, vol, u, red(c, R_DOT));
+  note(c);
+  sync_read(c, R_DOT, 1);
+  allreduce(c, R_DOT, 1);
+  return c->hred[R_DOT];
+}
+
+// energy (model.hpp:56-86)
+template <int DIM>
+static double energy_impl(okg_ctx* c, const double* u, int* cg_iters) {
+  const okg_params& p = c->p;
+  const size_t B = c->B;
+  apply_level<DIM>(c, 0, c->K, u, c->kv);
+  const double grad_term = 0.5 * p.eps * p.eps * dotv(c, u, c->kv);
+  const double well_term = 0.25 * double_well_impl<DIM>(c, u);
+  double nonlocal = 0.0;
+  if (cg_iters) *cg_iters = 0;
+  if (p.sigma != 0.0) {
+    double* rhs = c->r2p;
+    apply_level<DIM>(c, 0, c->M, u, rhs);
+    launch(c, k_add_load<DIM>, own(c->fine), BS, 0, c->fine, (const double*)c->b_tab, -p.m, (const double*)rhs, rhs);
+    note(c);
+    // mean of the rhs (compatibility of the pure-Neumann solve)
+    launch(c, k_fill, vblk(B), BS, 0, 1.0, F(c, c->zz), B);
+    note(c);
+    const double mean = dotv(c, rhs, c->zz);
+    if (std::abs(mean) > 1e-6)
+      THROW(OKG_EINCONSISTENT, "energy: potential right-hand side is not mean-zero (|sum| = %f)", std::abs(mean));
+    const double q = 1.0 / std::sqrt((double)c->fine.N);
+    launch(c, k_fill, vblk(B), BS, 0, q, F(c, c->zz), B);
+    note(c);
+    bool conv = false;
+    const int its = cg<DIM>(c, c->K, rhs, c->sy, 1e-10, 2000, c->zz, conv);
+    if (cg_iters) *cg_iters = its;
+    if (!conv) THROW(OKG_ENUMERICAL, "energy: potential solve did not converge");
+    nonlocal = 0.5 * p.sigma * dotv(c, c->sy, rhs);
+  }
+  return grad_term + well_term + nonlocal;
+}
+
+// initial_state (model.hpp:93-114): the context's state becomes (u0, w0) at t = 0
+template <int DIM>
+static void initial_state_impl(okg_ctx* c, int* cg_iters) {
+  const okg_params& p = c->p;
+  const size_t B = c->B;
+  launch(c, k_cos_ic<DIM>, own(c->fine), BS, 0, c->fine, c->h, p.m, c->u_old);
+  note(c);
+  double* rhs = c->kv;
+  apply_level<DIM>(c, 0, c->K, c->u_old, rhs);
+  scale(c, p.eps * p.eps, F(c, rhs), F(c, rhs), B);
+  launch(c, k_nonlinear<DIM>, own(c->fine), BS, 0, c->fine, c->nl, (const double*)c->u_old, c->rr);
+  note(c);
+  axpy(c, 1.0, F(c, c->rr), F(c, rhs), B);
+  bool conv = false;
+  const int its = cg<DIM>(c, c->M, rhs, c->w_old, 1e-12, 1000, nullptr, conv);
+  if (cg_iters) *cg_iters = its;
+  if (!conv) THROW(OKG_ENUMERICAL, "initial_state: mass solve did not converge");
+  CK(cudaStreamSynchronize(c->stream));
+  c->t = 0.0;
+  c->step = 0;
+}
+
 // ---- setup (make_schur_context, precond.hpp:126-181) ---------------------------------------
 template <int DIM>
 static void build(okg_ctx* c) {
@@ -1494,7 +1644,7 @@ static void build(okg_ctx* c) {
     // (halo 3 / 2: only on levels that are not split across slabs)
     if (p.mg_pre == 2 && p.mg_post == 2 && p.mg_fuse >= 0)
       for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l)
-        if ((p.mg_fuse == 1 || DIM == 2 || c->lv[l].g.n <= 32) && c->lv[l].gh == 0 &&
+        if ((p.mg_fuse >= 1 || DIM == 2 || c->lv[l].g.n <= 32) && c->lv[l].gh == 0 &&
             (c->lv[l].rep || S == 1))
           c->lv[l].fused = true;
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
@@ -2312,6 +2462,90 @@ int okg_newton_step_host(okg_ctx* c, const double* u_old, const double* w_old, d
                          okg_step_stats* stats) {
   if (!c || !u_old || !w_old || !u_new || !w_new) return fail(OKG_EINVAL, "okg_newton_step_host: null argument");
   return newton_all(c, u_old, w_old, u_new, w_new, stats);
+}
+
+// ---- diagnostics and initial state ------------------------------------------
+// u == NULL: the context's current state; else a host array of N doubles
+static const double* diag_input(okg_ctx* s, const double* u) {
+  if (!u) return s->u_old;
+  ensure_io(s);
+  put_owned(s, u, s->io_a, 1);
+  return s->io_a;
+}
+
+int okg_total_mass(okg_ctx* c, const double* u, double* mass) {
+  if (!c || !mass) return fail(OKG_EINVAL, "okg_total_mass: null argument");
+  double r0 = 0.0;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    const double v = DISPATCH(s, total_mass_impl, s, diag_input(s, u));
+    if (s->rank == 0) r0 = v;
+  });
+  if (st == OKG_OK) *mass = r0;
+  return st;
+}
+
+int okg_double_well(okg_ctx* c, const double* u, double* value) {
+  if (!c || !value) return fail(OKG_EINVAL, "okg_double_well: null argument");
+  double r0 = 0.0;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    const double v = DISPATCH(s, double_well_impl, s, diag_input(s, u));
+    if (s->rank == 0) r0 = v;
+  });
+  if (st == OKG_OK) *value = r0;
+  return st;
+}
+
+int okg_energy(okg_ctx* c, const double* u, double* energy, int32_t* cg_iters) {
+  if (!c || !energy) return fail(OKG_EINVAL, "okg_energy: null argument");
+  double r0 = 0.0;
+  int it0 = 0;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    int its = 0;
+    const double v = DISPATCH(s, energy_impl, s, diag_input(s, u), &its);
+    if (s->rank == 0) {
+      r0 = v;
+      it0 = its;
+    }
+  });
+  if (st == OKG_OK) {
+    *energy = r0;
+    if (cg_iters) *cg_iters = it0;
+  }
+  return st;
+}
+
+int okg_initial_state(okg_ctx* c, int32_t* cg_iters) {
+  if (!c) return fail(OKG_EINVAL, "okg_initial_state: null context");
+  int it0 = 0;
+  const int st = each_slab(c, [&](okg_ctx* s) {
+    int its = 0;
+    DISPATCH(s, initial_state_impl, s, &its);
+    if (s->rank == 0) it0 = its;
+  });
+  if (st == OKG_OK && cg_iters) *cg_iters = it0;
+  return st;
+}
+
+int okg_advance(okg_ctx* c, int32_t with_energy, okg_step_stats* stats) {
+  if (!c) return fail(OKG_EINVAL, "okg_advance: null context");
+  okg_step_stats st0;
+  int st = newton_all(c, nullptr, nullptr, nullptr, nullptr, &st0);
+  if (st != OKG_OK) return st;
+  // advance (model.hpp:218-227): diagnostics of the new state
+  double mass = 0.0, en = 0.0;
+  st = each_slab(c, [&](okg_ctx* s) {
+    const double m = DISPATCH(s, total_mass_impl, s, s->u_old);
+    const double e = with_energy ? DISPATCH(s, energy_impl, s, s->u_old, nullptr) : 0.0;
+    if (s->rank == 0) {
+      mass = m;
+      en = e;
+    }
+  });
+  if (st != OKG_OK) return st;
+  st0.mass = mass;
+  st0.energy = with_energy ? en : NAN;
+  if (stats) *stats = st0;
+  return OKG_OK;
 }
 
 int okg_clear_linearization(okg_ctx* c) {

@@ -61,9 +61,16 @@ int main() {
   {
     SchurContext ctx = make_schur_context(cfg);
     const size_t n = static_cast<size_t>(ctx.rows());
-    State s0{Vector(n), Vector(n, 0.0), 0.0, 0};
-    for (size_t i = 0; i < n; ++i) s0.u[i] = cfg.m + 0.01 * std::sin(0.37 * static_cast<double>(i));
+    // advance computes the energy, which needs a mean-consistent field (model.hpp:68-73)
+    State bad{Vector(n), Vector(n, 0.0), 0.0, 0};
+    for (size_t i = 0; i < n; ++i) bad.u[i] = cfg.m + 0.01 * std::sin(0.37 * static_cast<double>(i));
+    REQUIRE(throws<InconsistentState>([&] { advance(bad, ctx, cfg); }));
+    const State s0 = initial_state(ctx, cfg);  // model.hpp:93-114
+    REQUIRE(s0.step == 0 && s0.t == 0.0 && s0.u.size() == n);
+    REQUIRE(std::abs(total_mass(ctx, s0.u) - cfg.m) <= 1e-13);
     auto res = advance(s0, ctx, cfg);
+    REQUIRE(std::abs(res.second.mass - cfg.m) <= 1e-13);  // mass is conserved
+    REQUIRE(std::isfinite(res.second.energy) && res.second.energy <= energy(ctx, s0.u, cfg) + 1e-12);
     REQUIRE(res.second.converged);
     REQUIRE(res.second.newton_iters >= 1 && res.second.newton_iters <= 8);
     REQUIRE(res.second.gmres_iters.size() == static_cast<size_t>(res.second.newton_iters));

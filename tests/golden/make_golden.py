@@ -5,7 +5,8 @@ where /root/reference exists:
     make -C oracle ref && python tests/golden/make_golden.py
 
 Each case stores its seeded inputs and the reference's outputs for every
-operator on the Newton-solve path, one GMRES solve and two Newton timesteps
+operator on the Newton-solve path, one GMRES solve, two Newton timesteps, and
+ initial_state, total_mass, integrate_double_well and energy
 (BASELINE.json settings: sigma=100, theta=.5, dt=eps^2, GMRES(30) rtol 1e-10,
 newton_tol 1e-8, seeded IC of SURVEY.md 8(d), w0 = 0).
 """
@@ -94,6 +95,17 @@ def make(name, dim, n, m, eps, seed, min_coarse=None):
         out[f"newton{s}_gmres"] = np.array(st.gmres_iters)
         out[f"newton{s}_res"] = st.residual_norm
         u, w = un, wn2
+    # diagnostics and initial state: initial_state, then total_mass /
+    # integrate_double_well / energy at u0 and at the state after one Newton step from it
+    u0, w0, _ = o.initial_state()
+    out["init_u"], out["init_w"] = u0, w0
+    u1, w1, st = o.newton_solve(u0, w0)
+    out["init_step_u"], out["init_step_w"] = u1, w1
+    out["init_step_gmres"] = np.array(st.gmres_iters)
+    for tag, uu in (("u0", u0), ("u1", u1)):
+        out[f"mass_{tag}"] = o.total_mass(uu)
+        out[f"well_{tag}"] = o.double_well(uu)
+        out[f"energy_{tag}"] = o.energy(uu)[0]
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     print(name, "levels", out["levels"], "gmres", out["gmres_iters"],
           "newton", [out["newton0_gmres"].tolist(), out["newton1_gmres"].tolist()])

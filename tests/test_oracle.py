@@ -157,3 +157,48 @@ def test_mass_identity(port_lib):
     mn, mo = b @ a_u, b @ b_u
     rhs = (mn - mo) + p.dt * p.sigma * (p.theta * (mn - p.m * vol) + (1 - p.theta) * (mo - p.m * vol))
     assert abs(r1.sum() - rhs) <= 1e-12
+
+
+# ---- diagnostics and initial state ---------------------------------------
+@pytest.mark.parametrize("case", golden_cases())
+def test_port_diagnostics_match_reference_golden_bitwise(port_lib, case):
+    """initial_state / total_mass / integrate_double_well / energy of the port vs the
+    reference's own outputs (model.hpp:46-114, assembly.hpp:220-245)."""
+    g = load_golden(case)
+    o = po.Oracle(golden_params(g, "port"), "port")
+    u0, w0, its = o.initial_state()
+    assert np.array_equal(u0, g["init_u"]) and np.array_equal(w0, g["init_w"])
+    assert its > 0
+    u1, w1, st = o.newton_solve(u0, w0)
+    assert np.array_equal(u1, g["init_step_u"]) and np.array_equal(w1, g["init_step_w"])
+    for tag, uu in (("u0", u0), ("u1", u1)):
+        assert o.total_mass(uu) == float(g[f"mass_{tag}"])
+        assert o.double_well(uu) == float(g[f"well_{tag}"])
+        assert o.energy(uu)[0] == float(g[f"energy_{tag}"])
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("dim,n,m,sigma", [(2, 24, 0.2, 100.0), (3, 6, -0.1, 100.0), (2, 16, 0.0, 0.0)])
+def test_port_diagnostics_match_reference_live(port_lib, dim, n, m, sigma):
+    res = {}
+    for kind in ("ref", "port"):
+        o = po.Oracle(po.baseline_params(dim, n, m=m, kind=kind, sigma=sigma), kind)
+        u0, w0, _ = o.initial_state()
+        res[kind] = (u0, w0, o.total_mass(u0), o.double_well(u0), o.energy(u0)[0])
+    for a, b in zip(res["ref"], res["port"]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_diagnostics_kats(port_lib):
+    o = po.Oracle(po.baseline_params(2, 32, m=0.25, kind="port"), "port")
+    u0, w0, _ = o.initial_state()
+    # the cosine bump integrates to zero: b^T u0 = m (unit box)
+    assert abs(o.total_mass(u0) - 0.25) < 1e-14
+    # double well of a constant field c: (1 - c^2)^2
+    assert abs(o.double_well(np.full(o.n, 0.5)) - 0.5625) < 1e-14
+    # w0 solves M w0 = eps^2 K u0 + N(u0) to rtol 1e-12 (model.hpp:101-107)
+    rhs = o.params.eps ** 2 * o.apply(po.K, u0) + o.apply(po.NONLINEAR, u0)
+    assert np.linalg.norm(o.apply(po.M, w0) - rhs) <= 1e-11 * np.linalg.norm(rhs)
+    # energy needs a mean-consistent field (model.hpp:68-73)
+    with pytest.raises(po.OracleError, match="InconsistentState"):
+        o.energy(po.seeded_ic(o.n, 1, 0.25, "port"))
