@@ -123,6 +123,12 @@ int oko_energy(void* ctx, const double* u, double* energy, int* cg_iters);
 /* initial_state (model.hpp:93-114): u0 (cosine bump), w0 (mass solve) */
 int oko_initial_state(void* ctx, double* u, double* w, int* cg_iters);
 
+/* ---- output formats; the compiled reference only ---- */
+/* format_g17 (vtk.hpp:17-22) into buf (NUL-terminated) */
+int oko_format_g17(double x, char* buf, int len);
+/* write_vtk (vtk.hpp:28-66) of a dim/n mesh */
+int oko_write_vtk(int dim, int n, const double* u, const double* w, const char* path);
+
 /* builder-defined seeded IC, SURVEY.md section 8(d) (counter-based splitmix64) */
 void oko_seeded_ic(long nverts, unsigned long long seed, double m, double* u);
 

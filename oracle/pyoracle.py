@@ -95,6 +95,9 @@ def load(kind: str = "ref"):
     lib.oko_double_well.argtypes = [C.c_void_p, _dp, _dp]
     lib.oko_energy.argtypes = [C.c_void_p, _dp, _dp, _ip]
     lib.oko_initial_state.argtypes = [C.c_void_p, _dp, _dp, _ip]
+    if kind == "ref":
+        lib.oko_format_g17.argtypes = [C.c_double, C.c_char_p, C.c_int]
+        lib.oko_write_vtk.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_char_p]
     _loaded[kind] = lib
     return lib
 
@@ -288,3 +291,24 @@ class Oracle:
         it = C.c_int()
         _check(self.lib, self.lib.oko_initial_state(self.h, _p(u), _p(w), C.byref(it)))
         return u, w, it.value
+
+
+# ---- output formats of the compiled reference ----
+# (through oracle/_ref/okref_io in a subprocess: numpy in this process breaks the
+# reference's iostream/locale code)
+REF_IO = os.path.join(HERE, "_ref", "okref_io")
+
+
+def ref_format_g17(xs, workdir: str):
+    import subprocess
+    p = os.path.join(workdir, "fmt_in.bin")
+    np.ascontiguousarray(xs, dtype=np.float64).tofile(p)
+    out = subprocess.run([REF_IO, "fmt", p], capture_output=True, text=True, check=True)
+    return out.stdout.splitlines()
+
+
+def ref_write_vtk(dim: int, n: int, u, w, path: str, workdir: str) -> None:
+    import subprocess
+    p = os.path.join(workdir, "vtk_in.bin")
+    np.concatenate([np.asarray(u, np.float64), np.asarray(w, np.float64)]).tofile(p)
+    subprocess.run([REF_IO, "vtk", str(dim), str(n), p, path], capture_output=True, check=True)

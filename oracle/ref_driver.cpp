@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "okflow/assembly.hpp"
+#include "okflow/vtk.hpp"  // (driver.hpp needs the un-vendored nlohmann json.hpp: not built)
 #include "okflow/krylov.hpp"
 #include "okflow/mesh.hpp"
 #include "okflow/model.hpp"
@@ -379,6 +380,20 @@ int oko_initial_state(void* ctx, double* u, double* w, int* cg_iters) {
     vec_out(s.u, u);
     vec_out(s.w, w);
     if (cg_iters) *cg_iters = -1;
+  });
+}
+
+int oko_format_g17(double x, char* buf, int len) {
+  return guarded([&] {
+    const std::string s = format_g17(x);
+    std::snprintf(buf, (size_t)len, "%s", s.c_str());
+  });
+}
+
+int oko_write_vtk(int dim, int n, const double* u, const double* w, const char* path) {
+  return guarded([&] {
+    const StructuredMesh mesh = build_mesh(dim, n);
+    write_vtk(mesh, vec_in(u, mesh.num_vertices()), vec_in(w, mesh.num_vertices()), path);
   });
 }
 
