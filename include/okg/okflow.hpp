@@ -84,6 +84,10 @@ struct SolverConfig {
   int threads = 1;
   long max_dofs = 2000000;
   int device = 0;
+  std::vector<int> mesh_study_n = {32, 64, 128};  // study sweeps (driver.hpp:130-205)
+  std::vector<double> eps_list = {0.02, 0.01};
+  std::string output_dir = ".";
+  int snapshot_every = 0;  // VTK snapshots every k steps; 0 = never
   int nslabs = 1;          // x-plane slabs; > 1: one host thread + stream each
   bool slab_devices = false;  // slab r on device `device + r` (else all on `device`)
 
@@ -120,13 +124,39 @@ struct SolverConfig {
     p.slab_devices = slab_devices ? 1 : 0;
     return p;
   }
-  void validate() const {  // SolverConfig::validate
-    if (cheby_precond != "jacobi" && cheby_precond != "ssor")
-      throw ConfigError("config: cheby_precond must be 'jacobi' or 'ssor'");
-    if (n_steps < 0) throw ConfigError("config: n_steps must be nonnegative");
-    if (threads < 1) throw ConfigError("config: threads must be at least 1");
-    const okg_params p = to_params();
-    check(okg_validate_params(&p));
+  // SolverConfig::validate (params.hpp:67-116): the first violated constraint, in the
+  // reference's order and with its message
+  void validate() const {
+    auto bad = [](const std::string& m) { throw ConfigError("config: " + m); };
+    if (!(eps > 0.0)) bad("eps must be positive");
+    if (sigma < 0.0) bad("sigma must be nonnegative");
+    if (!(std::abs(m) < 1.0)) bad("mean m must satisfy |m| < 1");
+    if (!(theta > 0.0) || theta > 1.0) bad("theta must lie in (0, 1]");
+    if (!(dt > 0.0)) bad("dt must be positive");
+    if (n_steps < 0) bad("n_steps must be nonnegative");
+    if (dim != 2 && dim != 3) bad("dim must be 2 or 3");
+    if (n < 1) bad("n must be at least 1");
+    if (!(newton_tol > 0.0)) bad("newton_tol must be positive");
+    if (newton_maxit < 1) bad("newton_maxit must be at least 1");
+    if (!(gmres_tol > 0.0)) bad("gmres_tol must be positive");
+    if (gmres_maxit < 1) bad("gmres_maxit must be at least 1");
+    if (gmres_restart < 0) bad("gmres_restart must be nonnegative");
+    if (cheby_iters < 1) bad("cheby_iters must be at least 1");
+    if (cheby_precond != "jacobi" && cheby_precond != "ssor") bad("cheby_precond must be 'jacobi' or 'ssor'");
+    if (richardson_steps < 1) bad("richardson_steps must be at least 1");
+    if (mg_cycles < 1) bad("mg_cycles must be at least 1");
+    if (mg_pre < 0 || mg_post < 0 || mg_pre + mg_post < 1) bad("need at least one smoothing sweep per cycle");
+    if (!(mg_omega > 0.0) || !(mg_omega < 2.0)) bad("mg_omega must lie in (0, 2)");
+    if (min_coarse_size < 1) bad("min_coarse_size must be at least 1");
+    for (int sn : mesh_study_n)
+      if (sn < 1) bad("mesh_study_n entries must be >= 1");
+    for (double se : eps_list)
+      if (!(se > 0.0)) bad("eps_list entries must be positive");
+    if (threads < 1) bad("threads must be at least 1");
+    if (max_dofs < 1) bad("max_dofs must be at least 1");
+    if (snapshot_every < 0) bad("snapshot_every must be nonnegative");
+    if (num_vertices() > max_dofs)
+      bad("mesh has " + std::to_string(num_vertices()) + " vertices, exceeding max_dofs = " + std::to_string(max_dofs));
   }
 };
 

@@ -129,6 +129,9 @@ int oko_format_g17(double x, char* buf, int len);
 /* write_vtk (vtk.hpp:28-66) of a dim/n mesh */
 int oko_write_vtk(int dim, int n, const double* u, const double* w, const char* path);
 
+/* parse_config (config.hpp:114-236): dump of the parsed SolverConfig, key=value per line */
+int oko_parse_config(const char* path, char* out, int len);
+
 /* builder-defined seeded IC, SURVEY.md section 8(d) (counter-based splitmix64) */
 void oko_seeded_ic(long nverts, unsigned long long seed, double m, double* u);
 

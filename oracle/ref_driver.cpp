@@ -12,11 +12,13 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "okflow/assembly.hpp"
+#include "okflow/config.hpp"
 #include "okflow/vtk.hpp"  // (driver.hpp needs the un-vendored nlohmann json.hpp: not built)
 #include "okflow/krylov.hpp"
 #include "okflow/mesh.hpp"
@@ -394,6 +396,32 @@ int oko_write_vtk(int dim, int n, const double* u, const double* w, const char* 
   return guarded([&] {
     const StructuredMesh mesh = build_mesh(dim, n);
     write_vtk(mesh, vec_in(u, mesh.num_vertices()), vec_in(w, mesh.num_vertices()), path);
+  });
+}
+
+int oko_parse_config(const char* path, char* out, int len) {
+  return guarded([&] {
+    const RunManifest man = parse_config(path);
+    const SolverConfig& c = man.config;
+    std::ostringstream os;
+    auto d = [&](const char* k, double v) { os << k << '=' << format_g17(v) << '\n'; };
+    auto i = [&](const char* k, long v) { os << k << '=' << v << '\n'; };
+    d("eps", c.eps); d("sigma", c.sigma); d("m", c.m); d("theta", c.theta); d("dt", c.dt);
+    i("n_steps", c.n_steps); i("dim", c.dim); i("n", c.n); d("newton_tol", c.newton_tol);
+    i("newton_maxit", c.newton_maxit); d("gmres_tol", c.gmres_tol); i("gmres_maxit", c.gmres_maxit);
+    i("gmres_restart", c.gmres_restart); i("cheby_iters", c.cheby_iters);
+    os << "cheby_precond=" << c.cheby_precond << '\n';
+    i("richardson_steps", c.richardson_steps); i("mg_cycles", c.mg_cycles); i("mg_pre", c.mg_pre);
+    i("mg_post", c.mg_post); d("mg_omega", c.mg_omega); i("min_coarse_size", c.min_coarse_size);
+    i("threads", c.threads); i("max_dofs", c.max_dofs);
+    os << "output_dir=" << c.output_dir << '\n';
+    i("snapshot_every", c.snapshot_every);
+    os << "mesh_study_n=";
+    for (size_t q = 0; q < c.mesh_study_n.size(); ++q) os << (q ? "," : "") << c.mesh_study_n[q];
+    os << "\neps_list=";
+    for (size_t q = 0; q < c.eps_list.size(); ++q) os << (q ? "," : "") << format_g17(c.eps_list[q]);
+    os << '\n';
+    std::snprintf(out, (size_t)len, "%s", os.str().c_str());
   });
 }
 

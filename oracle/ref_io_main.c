@@ -3,7 +3,8 @@
  * from a process without numpy (numpy in the same process breaks the
  * reference's iostream/locale code).
  *   okref_io fmt IN.bin            one format_g17 line per double of IN.bin
- *   okref_io vtk DIM N IN.bin OUT  write_vtk of u, w = the two halves of IN.bin */
+ *   okref_io vtk DIM N IN.bin OUT  write_vtk of u, w = the two halves of IN.bin
+ *   okref_io cfg PATH              parse_config: the parsed values, or "ERR code: message" */
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -44,6 +45,13 @@ int main(int argc, char** argv) {
     }
     return 0;
   }
-  fprintf(stderr, "usage: okref_io fmt IN.bin | okref_io vtk DIM N IN.bin OUT\n");
+  if (argc == 3 && !strcmp(argv[1], "cfg")) {
+    static char out[1 << 16];
+    const int st = oko_parse_config(argv[2], out, sizeof out);
+    if (st) printf("ERR %d: %s\n", st, oko_last_error());
+    else fputs(out, stdout);
+    return 0;
+  }
+  fprintf(stderr, "usage: okref_io fmt IN.bin | okref_io vtk DIM N IN.bin OUT | okref_io cfg PATH\n");
   return 1;
 }

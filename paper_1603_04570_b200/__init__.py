@@ -65,6 +65,10 @@ class SolverConfig:
     min_coarse_size: int = 500
     threads: int = 1
     max_dofs: int = 2000000
+    mesh_study_n: List[int] = field(default_factory=lambda: [32, 64, 128])
+    eps_list: List[float] = field(default_factory=lambda: [0.02, 0.01])
+    output_dir: str = "."
+    snapshot_every: int = 0
 
     def num_vertices(self) -> int:
         s = self.n + 1
@@ -93,13 +97,39 @@ class SolverConfig:
         return p
 
     def validate(self) -> None:
-        """SolverConfig::validate (params.hpp:68-116): raises ConfigError."""
-        if self.cheby_precond not in ("jacobi", "ssor"):
-            raise ConfigError("config: cheby_precond must be 'jacobi' or 'ssor'")
-        if self.threads < 1:
-            raise ConfigError("config: threads must be at least 1")
-        if self.n_steps < 0:
-            raise ConfigError("config: n_steps must be nonnegative")
+        """SolverConfig::validate (params.hpp:67-116): the first violated constraint, in
+        the reference's order and with its message (ConfigError)."""
+        def bad(msg):
+            raise ConfigError("config: " + msg)
+        if not self.eps > 0.0: bad("eps must be positive")
+        if self.sigma < 0.0: bad("sigma must be nonnegative")
+        if not abs(self.m) < 1.0: bad("mean m must satisfy |m| < 1")
+        if not self.theta > 0.0 or self.theta > 1.0: bad("theta must lie in (0, 1]")
+        if not self.dt > 0.0: bad("dt must be positive")
+        if self.n_steps < 0: bad("n_steps must be nonnegative")
+        if self.dim not in (2, 3): bad("dim must be 2 or 3")
+        if self.n < 1: bad("n must be at least 1")
+        if not self.newton_tol > 0.0: bad("newton_tol must be positive")
+        if self.newton_maxit < 1: bad("newton_maxit must be at least 1")
+        if not self.gmres_tol > 0.0: bad("gmres_tol must be positive")
+        if self.gmres_maxit < 1: bad("gmres_maxit must be at least 1")
+        if self.gmres_restart < 0: bad("gmres_restart must be nonnegative")
+        if self.cheby_iters < 1: bad("cheby_iters must be at least 1")
+        if self.cheby_precond not in ("jacobi", "ssor"): bad("cheby_precond must be 'jacobi' or 'ssor'")
+        if self.richardson_steps < 1: bad("richardson_steps must be at least 1")
+        if self.mg_cycles < 1: bad("mg_cycles must be at least 1")
+        if self.mg_pre < 0 or self.mg_post < 0 or self.mg_pre + self.mg_post < 1:
+            bad("need at least one smoothing sweep per cycle")
+        if not self.mg_omega > 0.0 or not self.mg_omega < 2.0: bad("mg_omega must lie in (0, 2)")
+        if self.min_coarse_size < 1: bad("min_coarse_size must be at least 1")
+        if any(sn < 1 for sn in self.mesh_study_n): bad("mesh_study_n entries must be >= 1")
+        if any(not se > 0.0 for se in self.eps_list): bad("eps_list entries must be positive")
+        if self.threads < 1: bad("threads must be at least 1")
+        if self.max_dofs < 1: bad("max_dofs must be at least 1")
+        if self.snapshot_every < 0: bad("snapshot_every must be nonnegative")
+        if self.num_vertices() > self.max_dofs:
+            bad(f"mesh has {self.num_vertices()} vertices, exceeding max_dofs = {self.max_dofs}")
+        # and the same checks through the C ABI (okg_validate_params) for the solver fields
         check(lib.okg_validate_params(C.byref(self.to_params())))
 
 
