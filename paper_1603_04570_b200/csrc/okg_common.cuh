@@ -161,12 +161,18 @@ __device__ __forceinline__ double op_row(const Op<DIM>& op, const Grid& g, uint3
 #pragma unroll
     for (int o = 0; o < NO; ++o) s = fma(op.w[o], ld((uint32_t)((int)idx + g.off[o])), s);
   } else {
+    // boundary row: all weights, then all operands (a slot whose neighbour does not
+    // exist has weight 0 and reads the vertex itself), then the FMA chain -- two
+    // memory round trips instead of one per slot.  fma(0, v, s) == s up to the sign
+    // of a zero, so rows equal those that skip the zero slots.
     const double* t = op.tab + cls * (NO + 1);
+    double w[NO], v[NO];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const double w = __ldg(t + o);
-      if (w != 0.0) s = fma(w, ld((uint32_t)((int)idx + g.off[o])), s);
-    }
+    for (int o = 0; o < NO; ++o) w[o] = __ldg(t + o);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) v[o] = ld(w[o] != 0.0 ? (uint32_t)((int)idx + g.off[o]) : idx);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) s = fma(w[o], v[o], s);
   }
   return s;
 }

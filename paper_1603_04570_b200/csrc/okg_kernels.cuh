@@ -209,11 +209,13 @@ __global__ void __launch_bounds__(BS) k_restrict(Grid gf, Grid gc, const double*
 #pragma unroll
     for (int o = 0; o < NO; ++o)
       s += (o == Traits<DIM>::CENTER ? 1.0 : 0.5) * __ldg(rf + (int)F + gf.off[o]);
-  } else {
+  } else {  // branch-free: missing slots read the centre with weight 0 (see op_row)
+    double v[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) v[o] = __ldg(rf + (slot_ok<DIM>(nc.cls, o) ? (int)F + gf.off[o] : (int)F));
 #pragma unroll
     for (int o = 0; o < NO; ++o)
-      if (slot_ok<DIM>(nc.cls, o))
-        s += (o == Traits<DIM>::CENTER ? 1.0 : 0.5) * __ldg(rf + (int)F + gf.off[o]);
+      s += (slot_ok<DIM>(nc.cls, o) ? (o == Traits<DIM>::CENTER ? 1.0 : 0.5) : 0.0) * v[o];
   }
   rc[idx] = s;
 }
