@@ -175,15 +175,22 @@ __global__ void __launch_bounds__(BS) k_pre2(Grid g, Op<DIM> op, const double* _
 #pragma unroll
     for (int o = 0; o < NO; ++o) s = fma(op.w[o], wi * __ldg(r + (int)idx + g.off[o]), s);
   } else {
+    // branch-free (see op_row): weights, neighbour classes and operands first;
+    // missing / zero-weight slots read the vertex itself with weight 0
+    double w[NO], wi[NO], rv[NO];
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
-      if (!slot_ok<DIM>(nd.cls, o)) continue;
-      const double w = nd.cls == Traits<DIM>::INTERIOR ? op.w[o] : __ldg(op.tab + nd.cls * (NO + 1) + o);
-      if (w == 0.0) continue;
-      const uint32_t j = (uint32_t)((int)idx + g.off[o]);
-      const Node<DIM> nj = locate<DIM>(g, j);
-      s = fma(w, omega * op_invd<DIM>(op, nj.cls) * __ldg(r + j), s);
+      const bool ok = slot_ok<DIM>(nd.cls, o);
+      w[o] = !ok ? 0.0 : (nd.cls == Traits<DIM>::INTERIOR ? op.w[o] : __ldg(op.tab + nd.cls * (NO + 1) + o));
+      const int ci = ok ? cdig(nd.i + off_comp(DIM, o, 0), g.n) : cdig(nd.i, g.n);
+      const int cj = ok ? cdig(nd.j + off_comp(DIM, o, 1), g.n) : cdig(nd.j, g.n);
+      const int ck = DIM == 3 ? (ok ? cdig(nd.k + off_comp(DIM, o, 2), g.n) : cdig(nd.k, g.n)) : 0;
+      const int ncls = DIM == 3 ? ci * 9 + cj * 3 + ck : ci * 3 + cj;
+      wi[o] = op_invd<DIM>(op, ncls);
+      rv[o] = __ldg(r + (ok ? (int)idx + g.off[o] : (int)idx));
     }
+#pragma unroll
+    for (int o = 0; o < NO; ++o) s = fma(w[o], omega * wi[o] * rv[o], s);
   }
   const double wd = omega * op_invd<DIM>(op, nd.cls);
   const double ri = r[idx];

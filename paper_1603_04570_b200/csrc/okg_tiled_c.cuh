@@ -50,10 +50,14 @@ __device__ __forceinline__ void c_vertex(const Grid& g, const Op<DIM>& Mop, cons
   constexpr int NO = Traits<DIM>::NOFF;
   const bool inter = cls == Traits<DIM>::INTERIOR;
   double cx = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+  // all coefficients first (a missing slot reads the vertex's own array entry; its
+  // operand xs/vs is 0), so the loads are not serialised behind the FMA chain
+  double cf[NO];
+#pragma unroll
+  for (int o = 0; o < NO; ++o) cf[o] = c_coef<DIM>(a, idx, (inter || slot_ok<DIM>(cls, o)) ? g.off[o] : 0, o);
 #pragma unroll
   for (int o = 0; o < NO; ++o) {
-    if (!inter && !slot_ok<DIM>(cls, o)) continue;
-    cx = fma(c_coef<DIM>(a, idx, g.off[o], o), xs[o], cx);
+    cx = fma(cf[o], xs[o], cx);
     if (MODE == TC_ME) {
       const double kw = inter ? Kop.w[o] : __ldg(Kop.tab + cls * (NO + 1) + o);
       t1 = fma(kw, xs[o], t1);
