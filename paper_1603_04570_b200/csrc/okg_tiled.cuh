@@ -168,33 +168,46 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
     const uint32_t idx = __ldg(tl.bnd + t);
     const Node<DIM> nd = locate<DIM>(g, idx);
     const double* w = op.tab + nd.cls * (NO + 1);
-    // branch-free gather (see op_row): every slot loads -- a missing neighbour reads
-    // the vertex itself -- and is weighted by the class row (0 for missing slots)
-    double wv[NO], sv[NO];
+    double As = 0.0, s_own = 0.0;
+    if constexpr (LOAD == L_PROLONG) {
+      // per-slot loop (each staged value needs the coarse correction; the batched
+      // form below costs this kernel 16+ registers and a CTA per SM)
 #pragma unroll
-    for (int o = 0; o < NO; ++o) wv[o] = __ldg(w + o);
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const int di = off_comp(DIM, o, 0);
-      const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
-      const int dk = off_comp(DIM, o, DIM - 1);
-      int ni = nd.i + di;
-      int nj = DIM == 3 ? nd.j + dj : 0;
-      int nk = (DIM == 3 ? nd.k : nd.j) + dk;  // fastest coordinate
-      const bool ok = !(ni < 0 || ni > g.n || nk < 0 || nk > g.n || (DIM == 3 && (nj < 0 || nj > g.n)));
-      uint32_t v = (uint32_t)((int)idx + g.off[o]);
-      if (!ok) {
-        ni = nd.i;
-        nj = DIM == 3 ? nd.j : 0;
-        nk = DIM == 3 ? nd.k : nd.j;
-        v = idx;
+      for (int o = 0; o < NO; ++o) {
+        const int ni = nd.i + off_comp(DIM, o, 0);
+        const int nj = DIM == 3 ? nd.j + off_comp(DIM, o, 1) : 0;
+        const int nk = (DIM == 3 ? nd.k : nd.j) + off_comp(DIM, o, DIM - 1);  // fastest coordinate
+        if (ni < 0 || ni > g.n || nk < 0 || nk > g.n || (DIM == 3 && (nj < 0 || nj > g.n))) continue;
+        const double sv = stage_val<DIM, LOAD>(g, op, a, (uint32_t)((int)idx + g.off[o]), ni, nj, nk);
+        if (o == Traits<DIM>::CENTER) s_own = sv;
+        const double wo = __ldg(w + o);
+        if (wo != 0.0) As = fma(wo, sv, As);
       }
-      sv[o] = stage_val<DIM, LOAD>(g, op, a, v, ni, nj, nk);
-    }
-    double As = 0.0;
-    const double s_own = sv[Traits<DIM>::CENTER];
+    } else {
+      // branch-free gather (see op_row): every slot loads -- a missing neighbour reads
+      // the vertex itself -- and is weighted by the class row (0 for missing slots)
+      double wv[NO], sv[NO];
 #pragma unroll
-    for (int o = 0; o < NO; ++o) As = fma(wv[o], sv[o], As);
+      for (int o = 0; o < NO; ++o) wv[o] = __ldg(w + o);
+#pragma unroll
+      for (int o = 0; o < NO; ++o) {
+        int ni = nd.i + off_comp(DIM, o, 0);
+        int nj = DIM == 3 ? nd.j + off_comp(DIM, o, 1) : 0;
+        int nk = (DIM == 3 ? nd.k : nd.j) + off_comp(DIM, o, DIM - 1);  // fastest coordinate
+        const bool ok = !(ni < 0 || ni > g.n || nk < 0 || nk > g.n || (DIM == 3 && (nj < 0 || nj > g.n)));
+        uint32_t v = (uint32_t)((int)idx + g.off[o]);
+        if (!ok) {
+          ni = nd.i;
+          nj = DIM == 3 ? nd.j : 0;
+          nk = DIM == 3 ? nd.k : nd.j;
+          v = idx;
+        }
+        sv[o] = stage_val<DIM, LOAD>(g, op, a, v, ni, nj, nk);
+      }
+      s_own = sv[Traits<DIM>::CENTER];
+#pragma unroll
+      for (int o = 0; o < NO; ++o) As = fma(wv[o], sv[o], As);
+    }
     const double bv = EpiNeeds<EPI>::B ? a.b[idx] : 0.0;
     const double pv = EPI == T_CHEB ? a.x2[idx] : (EPI == T_JACOBI_ACC ? a.acc[idx] : 0.0);
     epilogue_pre<DIM, EPI>(a, idx, s_own, As, __ldg(w + NO), bv, pv);
