@@ -79,6 +79,8 @@ typedef struct okg_params {
                                device `device + r` (peer copies over NVLink) */
   int32_t tail_cluster;     /* CTAs in the tail's cluster (they split the rows of the dense
                                coarse inverse): 0 = default (enough for <= 96 KB each), 1..16 */
+  int32_t cheb_fuse;        /* Chebyshev steps two per pass (2D, one slab): 0 = default (on),
+                               < 0 = one step per pass */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */

@@ -45,7 +45,7 @@ class Params(C.Structure):
         ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
         ("tail_max_vertices", C.c_int32), ("disable_pdl", C.c_int32),
         ("mg_fuse", C.c_int32), ("nslabs", C.c_int32), ("slab_devices", C.c_int32),
-        ("tail_cluster", C.c_int32),
+        ("tail_cluster", C.c_int32), ("cheb_fuse", C.c_int32),
     ]
 
 

@@ -34,6 +34,7 @@
 #include "../../include/okg.h"
 #include "okg_kernels.cuh"
 #include "okg_diag.cuh"
+#include "okg_cheb2.cuh"
 #include "okg_nccl.h"
 #include "okg_tables.h"
 
@@ -137,6 +138,7 @@ struct okg_ctx {
   double *gb = nullptr, *gx = nullptr, *gr = nullptr, *pin = nullptr, *pz = nullptr, *pw = nullptr,
          *gt = nullptr;
   // preconditioner scratch
+  double* cr2 = nullptr;  // second Chebyshev residual buffer (two-step kernel, okg_cheb2.cuh)
   double *cd0 = nullptr, *cd1 = nullptr, *cr = nullptr, *r2p = nullptr, *sy = nullptr, *st = nullptr,
          *kv = nullptr, *zz = nullptr, *rr = nullptr, *z2 = nullptr, *shr = nullptr;
   // state
@@ -827,6 +829,38 @@ static void shat_inv(okg_ctx* c, const double* b, double* x, int cycles) {
   }
 }
 
+// two Chebyshev steps in one pass (2D only; okg_cheb2.cuh)
+template <int DIM>
+static void cheb2_launch(okg_ctx* c, const Op<DIM>& o, const Cheb2Args& a) {
+  if constexpr (DIM == 2) {
+    const Level& L = c->lv[0];
+    auto run = [&](auto TIc) {
+      constexpr int TI = decltype(TIc)::value;
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(k_cheb2<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cheb2_smem_bytes<TI>()));
+        attr = true;
+      }
+      // the level's tiling re-cut into TI-row chunks (same boundary list)
+      Tiling t = L.tl;
+      const int nci = std::max(0, t.ci1 - t.ci0);
+      t.ichunk = TI;
+      t.ncore = t.ktiles * ((nci + TI - 1) / TI);
+      const unsigned blocks = (unsigned)t.ncore + (t.nbnd + TileCfg<2>::NT - 1) / TileCfg<2>::NT;
+      launch(c, k_cheb2<TI>, blocks, TileCfg<2>::NT, cheb2_smem_bytes<TI>(), L.g, o, t, a);
+      note(c);
+    };
+    const int ti = c->p.cheb_fuse > 0 ? c->p.cheb_fuse : 4;  // rows per tile (measured best: see DESIGN)
+    if (ti >= 8) run(std::integral_constant<int, 8>{});
+    else if (ti >= 4) run(std::integral_constant<int, 4>{});
+    else run(std::integral_constant<int, 2>{});
+  } else {
+    (void)c;
+    (void)o;
+    (void)a;
+  }
+}
+
 // ---- Chebyshev (krylov.hpp:158-202) ---------------------------------------------
 template <int DIM>
 static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
@@ -841,10 +875,41 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
     copy(c, dcur + g.lo, x + g.lo, g.hi - g.lo);
     return;
   }
+  // 2D, one slab, tiled finest level: two steps per pass (okg_cheb2.cuh)
+  const bool two = DIM == 2 && c->lv[0].tiled && c->nslabs == 1 && c->p.cheb_fuse >= 0;
+  double* rcur = nullptr;  // r_j (b before the first step)
   for (int j = 0; j + 1 < k; ++j) {
     const int last = (j == k - 2);
+    if (two && j + 2 < k) {
+      Cheb2Args a2;
+      a2.d = dcur;
+      a2.r = j == 0 ? b : rcur;
+      a2.x = j == 0 ? dcur : x;
+      a2.d_out = dnxt;
+      a2.r_out = (rcur == c->cr) ? c->cr2 : c->cr;
+      a2.x_out = x;
+      a2.c1a = c->cheb_c1[j];
+      a2.c2a = c->cheb_c2[j];
+      a2.c1b = c->cheb_c1[j + 1];
+      a2.c2b = c->cheb_c2[j + 1];
+      a2.last = (j + 1 == k - 2);
+      cheb2_launch<DIM>(c, o, a2);
+      rcur = a2.r_out;
+      std::swap(dcur, dnxt);
+      ++j;  // two steps done
+      continue;
+    }
     exchange(c, 0, dcur);
-    if (c->lv[0].tiled) {
+    if (two) {  // a single step left over (odd count): reads rcur, writes the other buffer
+      TArgs a = targs(dcur, j == 0 ? b : rcur, (rcur == c->cr) ? c->cr2 : c->cr, x, 0.0);
+      a.x2 = j == 0 ? dcur : x;
+      a.y2 = dnxt;
+      a.c1 = c->cheb_c1[j];
+      a.c2 = c->cheb_c2[j];
+      a.last = last;
+      tiled<DIM, L_PLAIN, T_CHEB>(c, c->lv[0], A, a);
+      rcur = (rcur == c->cr) ? c->cr2 : c->cr;
+    } else if (c->lv[0].tiled) {
       TArgs a = targs(dcur, j == 0 ? b : c->cr, c->cr, x, 0.0);
       a.x2 = j == 0 ? dcur : x;
       a.y2 = dnxt;
@@ -1705,8 +1770,8 @@ static void build(okg_ctx* c) {
   c->vcap = cycle_len + 1;
   c->V = dalloc(c, (size_t)c->vcap * N2);
   for (double** b : {&c->gb, &c->gx, &c->gr, &c->pin, &c->pz, &c->pw, &c->gt}) *b = lvec(c, L0, 0, 2);
-  for (double** b : {&c->cd0, &c->cd1, &c->cr, &c->r2p, &c->sy, &c->st, &c->kv, &c->zz, &c->rr, &c->z2, &c->shr,
-                     &c->u_old, &c->w_old, &c->u, &c->w})
+  for (double** b : {&c->cd0, &c->cd1, &c->cr, &c->cr2, &c->r2p, &c->sy, &c->st, &c->kv, &c->zz, &c->rr, &c->z2,
+                     &c->shr, &c->u_old, &c->w_old, &c->u, &c->w})
     *b = lvec(c, L0, 0);
   // Chebyshev bounds and coefficients
   jacobi_spectrum<DIM>(c, c->lambda_lo, c->lambda_hi);
