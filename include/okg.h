@@ -81,6 +81,8 @@ typedef struct okg_params {
                                coarse inverse): 0 = default (enough for <= 96 KB each), 1..16 */
   int32_t cheb_fuse;        /* Chebyshev steps two per pass (2D, one slab): 0 = default (on),
                                < 0 = one step per pass */
+  int32_t cheby_ssor;       /* SolverConfig::cheby_precond: 0 = "jacobi", 1 = "ssor" (SSOR
+                               sweeps as hyperplane wavefronts, one slab only) */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -146,7 +148,8 @@ enum okg_op {
   OKG_OP_BLOCK = 15,         /* apply_block  (2N -> 2N)          precond.hpp:257       */
   OKG_OP_JACOBIAN = 16,      /* jacobian_operator (2N -> 2N)     precond.hpp:277       */
   OKG_OP_NONLINEAR = 17,     /* assemble_nonlinear(mesh, x)      assembly.hpp:194      */
-  OKG_OP_COARSE_SOLVE = 18   /* coarsest-level direct solve      dense.hpp:197         */
+  OKG_OP_COARSE_SOLVE = 18,  /* coarsest-level direct solve      dense.hpp:197         */
+  OKG_OP_SSOR_M = 19         /* SsorSweeps(M, 1).apply_inv       krylov.hpp:372-378    */
 };
 
 /* SolverConfig defaults (params.hpp:29-46) */

@@ -122,6 +122,7 @@ struct SolverConfig {
     p.device = device;
     p.nslabs = nslabs;
     p.slab_devices = slab_devices ? 1 : 0;
+    p.cheby_ssor = cheby_precond == "ssor" ? 1 : 0;
     return p;
   }
   // SolverConfig::validate (params.hpp:67-116): the first violated constraint, in the

@@ -37,6 +37,7 @@ typedef struct oko_params {
   double mg_omega;
   int min_coarse_size;
   double shat_perturb;
+  int cheby_ssor; /* cheby_precond: 0 = "jacobi", 1 = "ssor" (krylov.hpp:322-418) */
 } oko_params;
 
 /* operator kinds for oko_apply (level only used by SHAT/PROLONG/RESTRICT) */
@@ -59,7 +60,8 @@ enum {
   OKO_BLOCK = 15,       /* apply_block (2N -> 2N)          precond.hpp:257 */
   OKO_JACOBIAN = 16,    /* jacobian_operator (2N -> 2N)    precond.hpp:277 */
   OKO_NONLINEAR = 17,   /* assemble_nonlinear(mesh, x)     assembly.hpp:194 */
-  OKO_COARSE_SOLVE = 18 /* coarse_solver->solve (coarsest level)          */
+  OKO_COARSE_SOLVE = 18, /* coarse_solver->solve (coarsest level)         */
+  OKO_SSOR_M = 19        /* SsorSweeps(M, 1).apply_inv  krylov.hpp:372-378 */
 };
 
 /* status codes (negative) mirror the reference exception types, errors.hpp:9-28 */

@@ -732,22 +732,11 @@ static double mt_uniform(mt19937_t* g, double a, double b) {
   return ret * (b - a) + a;
 }
 
-/* lanczos_extremes (krylov.hpp:248-289) on B = D^-1/2 A D^-1/2 */
-static int estimate_jacobi_spectrum(const csr* A, double* lo_out, double* hi_out) {
-  const int probes = 30;
-  const unsigned seed = 1234u;
-  const long n = A->nr;
-  double* d = dalloc(n);
-  csr_diag(A, d);
-  double* dsqrt = dalloc(n);
-  for (long i = 0; i < n; ++i) {
-    if (d[i] <= 0.0) {
-      free(d);
-      free(dsqrt);
-      FAIL(OKO_ENUMERICAL, "estimate_jacobi_spectrum: non-positive diagonal");
-    }
-    dsqrt[i] = sqrt(d[i]);
-  }
+/* lanczos_extremes (krylov.hpp:248-289): extreme Ritz values of apply_B after
+ * `probes` steps of Lanczos with full reorthogonalisation from mt19937(seed) */
+typedef void (*apply_fn)(const void* ctx, const double* x, double* y);
+static int lanczos_extremes(apply_fn apply_B, const void* actx, long n, int probes, unsigned seed, double* lo,
+                            double* hi) {
   int steps = probes < n ? probes : (int)n;
   mt19937_t rng;
   mt_seed(&rng, seed);
@@ -759,12 +748,9 @@ static int estimate_jacobi_spectrum(const csr* A, double* lo_out, double* hi_out
   V[nV++] = v;
   double alpha[64], beta[64];
   int na = 0, nb_ = 0;
-  double* t = dalloc(n);
   double* w = dalloc(n);
   for (int j = 0; j < steps; ++j) {
-    for (long i = 0; i < n; ++i) t[i] = V[j][i] / dsqrt[i];
-    spmv(A, t, w);
-    for (long i = 0; i < n; ++i) w[i] /= dsqrt[i];
+    apply_B(actx, V[j], w);
     const double a = dot(w, V[j], n);
     alpha[na++] = a;
     axpy(-a, V[j], w, n);
@@ -793,15 +779,154 @@ static int estimate_jacobi_spectrum(const csr* A, double* lo_out, double* hi_out
   for (int qv = 0; qv < nV; ++qv) free(V[qv]);
   free(V);
   free(T);
-  free(t);
   free(w);
+  if (st != OKO_OK) return st;
+  *lo = ev[0];
+  *hi = ev[mm - 1];
+  return OKO_OK;
+}
+
+typedef struct {
+  const csr* A;
+  const double* dsqrt;
+  double* t;
+} jacobi_probe_t;
+
+/* B = D^-1/2 A D^-1/2 (krylov.hpp:307-312) */
+static void jacobi_probe(const void* ctx, const double* x, double* y) {
+  const jacobi_probe_t* q = (const jacobi_probe_t*)ctx;
+  const long n = q->A->nr;
+  for (long i = 0; i < n; ++i) q->t[i] = x[i] / q->dsqrt[i];
+  spmv(q->A, q->t, y);
+  for (long i = 0; i < n; ++i) y[i] /= q->dsqrt[i];
+}
+
+/* estimate_jacobi_spectrum (krylov.hpp:296-320) */
+static int estimate_jacobi_spectrum(const csr* A, double* lo_out, double* hi_out) {
+  const long n = A->nr;
+  double* d = dalloc(n);
+  csr_diag(A, d);
+  double* dsqrt = dalloc(n);
+  for (long i = 0; i < n; ++i) {
+    if (d[i] <= 0.0) {
+      free(d);
+      free(dsqrt);
+      FAIL(OKO_ENUMERICAL, "estimate_jacobi_spectrum: non-positive diagonal");
+    }
+    dsqrt[i] = sqrt(d[i]);
+  }
+  jacobi_probe_t q = {A, dsqrt, dalloc(n)};
+  double lo = 0, hi = 0;
+  const int st = lanczos_extremes(jacobi_probe, &q, n, 30, 1234u, &lo, &hi);
+  free(q.t);
   free(d);
   free(dsqrt);
   if (st != OKO_OK) return st;
-  if (ev[0] < 0.0)
+  if (lo < 0.0)
     FAIL(OKO_ENUMERICAL, "estimate_jacobi_spectrum: negative Ritz value, matrix not positive definite");
-  *lo_out = 0.9 * ev[0];
-  *hi_out = 1.1 * ev[mm - 1];
+  *lo_out = 0.9 * lo;
+  *hi_out = 1.1 * hi;
+  return OKO_OK;
+}
+
+/* ---- SsorSweeps (krylov.hpp:322-388), omega = 1 as make_schur_context uses it ---- */
+typedef struct {
+  const csr* A;
+  double omega;
+  double* diag;
+} ssor_t;
+
+static int ssor_init(const csr* A, double omega, ssor_t* s) {
+  if (omega <= 0.0 || omega >= 2.0) FAIL(OKO_EINVAL, "ssor: omega must lie in (0, 2)");
+  s->A = A;
+  s->omega = omega;
+  s->diag = dalloc(A->nr);
+  csr_diag(A, s->diag);
+  for (long i = 0; i < A->nr; ++i)
+    if (s->diag[i] <= 0.0) FAIL(OKO_EINVAL, "ssor: non-positive diagonal");
+  return OKO_OK;
+}
+
+/* (D/w + L) x = r by forward substitution */
+static void ssor_forward(const ssor_t* s, const double* r, double* x) {
+  const csr* A = s->A;
+  for (int i = 0; i < A->nr; ++i) {
+    double acc = r[i];
+    for (int k = A->rp[i]; k < A->rp[i + 1]; ++k) {
+      const int j = A->ci[k];
+      if (j >= i) break;
+      acc -= A->v[k] * x[j];
+    }
+    x[i] = acc * s->omega / s->diag[i];
+  }
+}
+
+/* (D/w + U) x = r by backward substitution */
+static void ssor_backward(const ssor_t* s, const double* r, double* x) {
+  const csr* A = s->A;
+  for (int i = A->nr - 1; i >= 0; --i) {
+    double acc = r[i];
+    for (int k = A->rp[i + 1] - 1; k >= A->rp[i]; --k) {
+      const int j = A->ci[k];
+      if (j <= i) break;
+      acc -= A->v[k] * x[j];
+    }
+    x[i] = acc * s->omega / s->diag[i];
+  }
+}
+
+/* z = P^{-1} r (apply_inv) */
+static void ssor_apply_inv(const ssor_t* s, const double* r, double* z, double* t) {
+  ssor_forward(s, r, t);
+  const double g = (2.0 - s->omega) / s->omega;
+  for (long i = 0; i < s->A->nr; ++i) t[i] *= g * s->diag[i];
+  ssor_backward(s, t, z);
+}
+
+typedef struct {
+  const ssor_t* sw;
+  const double* dsqrt;
+  double g;
+  double *t, *u, *v;
+} ssor_probe_t;
+
+/* B = E A E^T with E = g D^{1/2} (D/w + L)^{-1} (krylov.hpp:400-407) */
+static void ssor_probe(const void* ctx, const double* x, double* y) {
+  const ssor_probe_t* q = (const ssor_probe_t*)ctx;
+  const long n = q->sw->A->nr;
+  for (long i = 0; i < n; ++i) q->t[i] = q->g * q->dsqrt[i] * x[i];
+  ssor_backward(q->sw, q->t, q->u);
+  spmv(q->sw->A, q->u, q->v);
+  ssor_forward(q->sw, q->v, y);
+  for (long i = 0; i < n; ++i) y[i] *= q->g * q->dsqrt[i];
+}
+
+/* estimate_ssor_spectrum (krylov.hpp:390-418) */
+static int estimate_ssor_spectrum(const csr* A, double omega, double* lo_out, double* hi_out) {
+  ssor_t sw;
+  TRY(ssor_init(A, omega, &sw));
+  const long n = A->nr;
+  ssor_probe_t q;
+  q.sw = &sw;
+  q.g = sqrt((2.0 - omega) / omega);
+  double* dsqrt = dalloc(n);
+  for (long i = 0; i < n; ++i) dsqrt[i] = sqrt(sw.diag[i]);
+  q.dsqrt = dsqrt;
+  q.t = dalloc(n);
+  q.u = dalloc(n);
+  q.v = dalloc(n);
+  double lo = 0, hi = 0;
+  const int st = lanczos_extremes(ssor_probe, &q, n, 30, 1234u, &lo, &hi);
+  free(q.t);
+  free(q.u);
+  free(q.v);
+  free(dsqrt);
+  free(sw.diag);
+  if (st != OKO_OK) return st;
+  if (lo < 0.0)
+    FAIL(OKO_ENUMERICAL, "estimate_ssor_spectrum: negative Ritz value, matrix not positive definite");
+  *lo_out = 0.9 * lo;
+  *hi_out = 1.1 * hi;
   return OKO_OK;
 }
 
@@ -950,6 +1075,8 @@ typedef struct {
   double* a_inv_diag;
   double lambda_lo, lambda_hi;
   hier_t h;
+  int ssor;          /* cheby_precond == "ssor" (precond.hpp:156-161) */
+  ssor_t m_sw, a_sw; /* SsorSweeps(M, 1), SsorSweeps(a_mat, 1) */
 } port_ctx;
 
 /* compute_c (precond.hpp:31-38) */
@@ -962,7 +1089,16 @@ static int compute_c(double dt, double theta, double sigma, double* c) {
 }
 
 /* chebyshev_semi_iteration (krylov.hpp:158-202) with Jacobi P_inv (precond.hpp:99-119) */
-static int chebyshev(const csr* A, const double* inv_diag, const double* b, int k, double lmin,
+/* z = P^{-1} r: Jacobi (inv_diag) or SSOR (sw, with scratch t) -- cheby_mass_solve,
+ * precond.hpp:99-119 */
+static void precond_apply(const double* inv_diag, const ssor_t* sw, const double* r, double* z, double* t,
+                          long n) {
+  if (sw) ssor_apply_inv(sw, r, z, t);
+  else
+    for (long i = 0; i < n; ++i) z[i] = r[i] * inv_diag[i];
+}
+
+static int chebyshev(const csr* A, const double* inv_diag, const ssor_t* sw, const double* b, int k, double lmin,
                      double lmax, double* x) {
   const long n = A->nr;
   if (lmin <= 0.0) FAIL(OKO_EINVAL, "chebyshev: lambda_min must be positive");
@@ -976,14 +1112,15 @@ static int chebyshev(const csr* A, const double* inv_diag, const double* b, int 
   double* z = dalloc(n);
   double* d = dalloc(n);
   double* Ad = dalloc(n);
-  for (long i = 0; i < n; ++i) z[i] = r[i] * inv_diag[i];
+  double* t = dalloc(n);
+  precond_apply(inv_diag, sw, r, z, t, n);
   for (long i = 0; i < n; ++i) d[i] = z[i] * (1.0 / theta);
   if (delta <= 1e-300) {
     for (int j = 0; j < k; ++j) {
       axpy(1.0, d, x, n);
       spmv(A, d, Ad);
       axpy(-1.0, Ad, r, n);
-      for (long i = 0; i < n; ++i) z[i] = r[i] * inv_diag[i];
+      precond_apply(inv_diag, sw, r, z, t, n);
       for (long i = 0; i < n; ++i) d[i] = z[i] * (1.0 / theta);
     }
   } else {
@@ -994,7 +1131,7 @@ static int chebyshev(const csr* A, const double* inv_diag, const double* b, int 
       if (j + 1 == k) break;
       spmv(A, d, Ad);
       axpy(-1.0, Ad, r, n);
-      for (long i = 0; i < n; ++i) z[i] = r[i] * inv_diag[i];
+      precond_apply(inv_diag, sw, r, z, t, n);
       const double rho_next = 1.0 / (2.0 * sigma1 - rho);
       for (long i = 0; i < n; ++i) d[i] = rho_next * rho * d[i] + 2.0 * rho_next / delta * z[i];
       rho = rho_next;
@@ -1004,14 +1141,17 @@ static int chebyshev(const csr* A, const double* inv_diag, const double* b, int 
   free(z);
   free(d);
   free(Ad);
+  free(t);
   return OKO_OK;
 }
 
 static int apply_M_inv(port_ctx* c, const double* r, double* x) {
-  return chebyshev(&c->M, c->m_inv_diag, r, c->p.cheby_iters, c->lambda_lo, c->lambda_hi, x);
+  return chebyshev(&c->M, c->m_inv_diag, c->ssor ? &c->m_sw : NULL, r, c->p.cheby_iters, c->lambda_lo,
+                   c->lambda_hi, x);
 }
 static int apply_A_inv(port_ctx* c, const double* r, double* x) {
-  return chebyshev(&c->A, c->a_inv_diag, r, c->p.cheby_iters, c->lambda_lo, c->lambda_hi, x);
+  return chebyshev(&c->A, c->a_inv_diag, c->ssor ? &c->a_sw : NULL, r, c->p.cheby_iters, c->lambda_lo,
+                   c->lambda_hi, x);
 }
 
 /* apply_schur_tilde_inv (precond.hpp:199-205) */
@@ -1403,6 +1543,7 @@ void oko_default_params(oko_params* p) {
   p->mg_omega = 2.0 / 3.0;
   p->min_coarse_size = 500;
   p->shat_perturb = 0.0;
+  p->cheby_ssor = 0;
 }
 
 static void ctx_free(port_ctx* c) {
@@ -1414,6 +1555,8 @@ static void ctx_free(port_ctx* c) {
   free(c->b);
   free(c->m_inv_diag);
   free(c->a_inv_diag);
+  free(c->m_sw.diag);
+  free(c->a_sw.diag);
   hier_free(&c->h);
   free(c);
 }
@@ -1447,7 +1590,14 @@ static int create(const oko_params* p, port_ctx* c) {
   c->dt_theta = p->dt * p->theta;
   c->shat_scale = scale_factor;
   csr_scale(&c->M, c->a_coeff, &c->A);
-  TRY(estimate_jacobi_spectrum(&c->M, &c->lambda_lo, &c->lambda_hi));
+  c->ssor = p->cheby_ssor != 0;
+  if (c->ssor) {  /* precond.hpp:156-161 */
+    TRY(estimate_ssor_spectrum(&c->M, 1.0, &c->lambda_lo, &c->lambda_hi));
+    TRY(ssor_init(&c->M, 1.0, &c->m_sw));
+    TRY(ssor_init(&c->A, 1.0, &c->a_sw));
+  } else {
+    TRY(estimate_jacobi_spectrum(&c->M, &c->lambda_lo, &c->lambda_hi));
+  }
   TRY(positive_inverse_diagonal(&c->M, &c->m_inv_diag));
   TRY(positive_inverse_diagonal(&c->A, &c->a_inv_diag));
   TRY(build_hierarchy(&c->mesh, &c->M, &c->K, c->shat_scale * c->eps * c->sqrt_c,
@@ -1549,6 +1699,15 @@ int oko_apply(void* ctx, int kind, int level, const double* x, double* y) {
     case OKO_JACOBIAN: return apply_jacobian(c, x, y);
     case OKO_NONLINEAR: assemble_nonlinear(&c->mesh, x, y); return OKO_OK;
     case OKO_COARSE_SOLVE: chol_solve(&h->coarse, x, y); return OKO_OK;
+    case OKO_SSOR_M: {
+      ssor_t sw;
+      TRY(ssor_init(&c->M, 1.0, &sw));
+      double* t = dalloc(c->mesh.nv);
+      ssor_apply_inv(&sw, x, y, t);
+      free(t);
+      free(sw.diag);
+      return OKO_OK;
+    }
     default: FAIL(OKO_EINVAL, "oko_apply: unknown kind");
   }
 }

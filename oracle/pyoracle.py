@@ -22,6 +22,7 @@ LIBS = {
 M, K, A, SHAT, PROLONG, RESTRICT, VCYCLE, SHAT_INV, CHEB_M, CHEB_A = range(10)
 ME, C_OP, SCHUR, SCHUR_TILDE_INV, S_INV_APPROX, BLOCK, JACOBIAN, NONLINEAR = range(10, 18)
 COARSE_SOLVE = 18
+SSOR_M = 19
 
 ERRORS = {
     -1: ValueError,
@@ -52,7 +53,7 @@ class Params(C.Structure):
         ("cheby_iters", C.c_int), ("richardson_steps", C.c_int),
         ("mg_cycles", C.c_int), ("mg_pre", C.c_int), ("mg_post", C.c_int),
         ("mg_omega", C.c_double), ("min_coarse_size", C.c_int),
-        ("shat_perturb", C.c_double),
+        ("shat_perturb", C.c_double), ("cheby_ssor", C.c_int),
     ]
 
 

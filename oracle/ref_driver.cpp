@@ -91,6 +91,7 @@ SolverConfig to_cfg(const oko_params& p) {
   c.mg_post = p.mg_post;
   c.mg_omega = p.mg_omega;
   c.min_coarse_size = p.min_coarse_size;
+  c.cheby_precond = p.cheby_ssor ? "ssor" : "jacobi";
   return c;
 }
 
@@ -125,6 +126,7 @@ void oko_default_params(oko_params* p) {
   p->mg_omega = c.mg_omega;
   p->min_coarse_size = c.min_coarse_size;
   p->shat_perturb = 0.0;
+  p->cheby_ssor = c.cheby_precond == "ssor" ? 1 : 0;
 }
 
 const char* oko_last_error(void) { return g_err.c_str(); }
@@ -262,6 +264,11 @@ int oko_apply(void* ctx, int kind, int level, const double* x, double* y) {
       case OKO_COARSE_SOLVE: {
         const long nc = h.ops.back().rows();
         vec_out(h.coarse_solver->solve(vec_in(x, nc)), y);
+        break;
+      }
+      case OKO_SSOR_M: {  // SsorSweeps(M, 1).apply_inv (krylov.hpp:372-378)
+        const SsorSweeps sw(r->ops.M, 1.0);
+        vec_out(sw.apply_inv(vec_in(x, n)), y);
         break;
       }
       default:

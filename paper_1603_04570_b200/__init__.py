@@ -95,6 +95,7 @@ class SolverConfig:
         p.slab_devices = 1 if slab_devices else 0
         p.tail_cluster = tail_cluster
         p.cheb_fuse = cheb_fuse
+        p.cheby_ssor = 1 if self.cheby_precond == "ssor" else 0
         return p
 
     def validate(self) -> None:
@@ -294,8 +295,6 @@ class SchurContext:
         `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
         process owning slab `rank`; host arrays stay full-size, the rank reads/writes its
         own planes."""
-        if cfg.cheby_precond != "jacobi":
-            raise ConfigError("schur context: only cheby_precond = 'jacobi' is implemented on the GPU path")
         self.cfg = cfg
         self.device = device
         self.handle = C.c_void_p()

@@ -24,7 +24,7 @@ OKG_EOTHER = -9
 
 OP_M, OP_K, OP_A, OP_SHAT, OP_PROLONG, OP_RESTRICT, OP_VCYCLE, OP_SHAT_INV = range(8)
 OP_CHEB_M, OP_CHEB_A, OP_ME, OP_C, OP_SCHUR, OP_SCHUR_TILDE_INV = range(8, 14)
-OP_S_INV_APPROX, OP_BLOCK, OP_JACOBIAN, OP_NONLINEAR, OP_COARSE_SOLVE = range(14, 19)
+OP_S_INV_APPROX, OP_BLOCK, OP_JACOBIAN, OP_NONLINEAR, OP_COARSE_SOLVE, OP_SSOR_M = range(14, 20)
 
 OKG_MAX_NEWTON = 64
 
@@ -46,6 +46,7 @@ class Params(C.Structure):
         ("tail_max_vertices", C.c_int32), ("disable_pdl", C.c_int32),
         ("mg_fuse", C.c_int32), ("nslabs", C.c_int32), ("slab_devices", C.c_int32),
         ("tail_cluster", C.c_int32), ("cheb_fuse", C.c_int32),
+        ("cheby_ssor", C.c_int32),
     ]
 
 

@@ -35,6 +35,7 @@
 #include "okg_kernels.cuh"
 #include "okg_diag.cuh"
 #include "okg_cheb2.cuh"
+#include "okg_ssor.cuh"
 #include "okg_nccl.h"
 #include "okg_tables.h"
 
@@ -139,6 +140,9 @@ struct okg_ctx {
          *gt = nullptr;
   // preconditioner scratch
   double* cr2 = nullptr;  // second Chebyshev residual buffer (two-step kernel, okg_cheb2.cuh)
+  double* cad = nullptr;  // A d of the SSOR-preconditioned Chebyshev
+  bool ssor = false;      // cheby_precond == "ssor" (okg_ssor.cuh)
+  int ssor_cluster = 1;   // CTAs of the sweep kernels' cluster
   double *cd0 = nullptr, *cd1 = nullptr, *cr = nullptr, *r2p = nullptr, *sy = nullptr, *st = nullptr,
          *kv = nullptr, *zz = nullptr, *rr = nullptr, *z2 = nullptr, *shr = nullptr;
   // state
@@ -829,6 +833,9 @@ static void shat_inv(okg_ctx* c, const double* b, double* x, int cycles) {
   }
 }
 
+template <int DIM>
+static void cheb_ssor(okg_ctx* c, const HostOp& A, const double* b, double* x);
+
 // two Chebyshev steps in one pass (2D only; okg_cheb2.cuh)
 template <int DIM>
 static void cheb2_launch(okg_ctx* c, const Op<DIM>& o, const Cheb2Args& a) {
@@ -864,6 +871,10 @@ static void cheb2_launch(okg_ctx* c, const Op<DIM>& o, const Cheb2Args& a) {
 // ---- Chebyshev (krylov.hpp:158-202) ---------------------------------------------
 template <int DIM>
 static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
+  if (c->ssor) {
+    cheb_ssor<DIM>(c, A, b, x);
+    return;
+  }
   const Grid& g = c->fine;
   const Op<DIM> o = dev_op<DIM>(A);
   const int k = c->p.cheby_iters;
@@ -1334,8 +1345,10 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
 // ---- Lanczos bounds (krylov.hpp:248-320) ------------------------------------------------
 // Same start vector as the reference (std::mt19937(1234), uniform(-1,1) over
 // the GLOBAL vertex order; each slab keeps its slice); dots allreduced.
-template <int DIM>
-static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
+// lanczos_extremes (krylov.hpp:248-289) of `apply_B` (y = B x on level-0 vectors),
+// widened x0.9 / x1.1 as the estimate_*_spectrum callers do; `what` names the caller
+template <int DIM, class ApplyB>
+static void lanczos_bounds(okg_ctx* c, ApplyB&& apply_B, const char* what, double& lo, double& hi) {
   const Level& L0 = c->lv[0];
   const uint64_t Nglob = L0.g.N;
   const size_t nloc = L0.g.hi - L0.g.lo, B = L0.B;
@@ -1377,8 +1390,7 @@ static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
   double* w = blk(need - 1);
   std::vector<double> alpha, beta;
   for (int j = 0; j < steps; ++j) {
-    exchange(c, 0, Vv[j]);
-    op_apply<DIM>(c, c->fine, c->M, EPI_SCALE_APPLY, Vv[j], nullptr, w, nullptr);
+    apply_B(Vv[j], w);
     const double a = dot(w, Vv[j]);
     alpha.push_back(a);
     axpy(c, -a, F(c, Vv[j]), F(c, w), B);
@@ -1407,10 +1419,86 @@ static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
     }
   }
   if (!symmetric_eigenvalues(T, m, ev)) THROW(OKG_ENUMERICAL, "symmetric eigensolver failed to converge");
-  if (ev.front() < 0.0)
-    THROW(OKG_ENUMERICAL, "estimate_jacobi_spectrum: negative Ritz value, matrix not positive definite");
+  if (ev.front() < 0.0) THROW(OKG_ENUMERICAL, "%s: negative Ritz value, matrix not positive definite", what);
   lo = 0.9 * ev.front();
   hi = 1.1 * ev.back();
+}
+
+// estimate_jacobi_spectrum(M) (krylov.hpp:296-320): B = D^-1/2 M D^-1/2
+template <int DIM>
+static void jacobi_spectrum(okg_ctx* c, double& lo, double& hi) {
+  lanczos_bounds<DIM>(
+      c,
+      [&](double* x, double* y) {
+        exchange(c, 0, x);
+        op_apply<DIM>(c, c->fine, c->M, EPI_SCALE_APPLY, x, nullptr, y, nullptr);
+      },
+      "estimate_jacobi_spectrum", lo, hi);
+}
+
+// ---- SSOR (cheby_precond = "ssor", okg_ssor.cuh) ---------------------------------
+// one sweep over the hyperplanes as one thread-block cluster
+template <int DIM, bool FWD>
+static void ssor_sweep(okg_ctx* c, const HostOp& A, const double* r, double* x) {
+  launch_cluster(c, k_ssor_sweep<DIM, FWD>, (unsigned)c->ssor_cluster, SSOR_NT, 0, c->fine, dev_op<DIM>(A), 1.0, r, x);
+  note(c);
+}
+
+// z = P_ssor^{-1} r = backward((2-w)/w D forward(r)), w = 1 (krylov.hpp:372-378); t scratch
+template <int DIM>
+static void ssor_apply(okg_ctx* c, const HostOp& A, const double* r, double* z, double* t) {
+  ssor_sweep<DIM, true>(c, A, r, t);
+  launch(c, k_diag_scale<DIM, false>, own(c->fine), 256, 0, c->fine, dev_op<DIM>(A), (2.0 - 1.0) / 1.0,
+         (const double*)t, t);
+  note(c);
+  ssor_sweep<DIM, false>(c, A, t, z);
+}
+
+// estimate_ssor_spectrum(M) (krylov.hpp:390-418): B = E M E^T, E = g D^1/2 (D/w + L)^-1
+template <int DIM>
+static void ssor_spectrum(okg_ctx* c, double& lo, double& hi) {
+  const double g = std::sqrt((2.0 - 1.0) / 1.0);
+  const Op<DIM> m = dev_op<DIM>(c->M);
+  lanczos_bounds<DIM>(
+      c,
+      [&](double* x, double* y) {
+        launch(c, k_diag_scale<DIM, true>, own(c->fine), 256, 0, c->fine, m, g, (const double*)x, c->cr2);
+        note(c);
+        ssor_sweep<DIM, false>(c, c->M, c->cr2, c->cd0);
+        apply_level<DIM>(c, 0, c->M, c->cd0, c->cd1);
+        ssor_sweep<DIM, true>(c, c->M, c->cd1, y);
+        launch(c, k_diag_scale<DIM, true>, own(c->fine), 256, 0, c->fine, m, g, (const double*)y, y);
+        note(c);
+      },
+      "estimate_ssor_spectrum", lo, hi);
+}
+
+// chebyshev_semi_iteration with the SSOR preconditioner (krylov.hpp:158-202 via
+// cheby_mass_solve, precond.hpp:99-119)
+template <int DIM>
+static void cheb_ssor(okg_ctx* c, const HostOp& A, const double* b, double* x) {
+  const size_t B = c->B;
+  const int k = c->p.cheby_iters;
+  const double lmin = c->lambda_lo, lmax = c->lambda_hi;
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+  double *r = c->cr, *z = c->cd1, *d = c->cd0, *t = c->cr2, *Ad = c->cad;
+  CK(cudaMemsetAsync(F(c, x), 0, B * sizeof(double), c->stream));
+  copy(c, F(c, b), F(c, r), B);
+  ssor_apply<DIM>(c, A, r, z, t);
+  scale(c, 1.0 / theta, F(c, z), F(c, d), B);
+  for (int j = 0; j < k; ++j) {
+    axpy(c, 1.0, F(c, d), F(c, x), B);
+    if (delta > 1e-300 && j + 1 == k) break;  // last correction applied
+    apply_level<DIM>(c, 0, A, d, Ad);
+    axpy(c, -1.0, F(c, Ad), F(c, r), B);
+    ssor_apply<DIM>(c, A, r, z, t);
+    if (delta <= 1e-300) {  // point spectrum: plain Richardson steps
+      scale(c, 1.0 / theta, F(c, z), F(c, d), B);
+    } else {
+      launch(c, k_lincomb, vblk(B), 256, 0, c->cheb_c1[j], F(c, d), c->cheb_c2[j], (const double*)F(c, z), B);
+      note(c);
+    }
+  }
 }
 
 // ---- diagnostics and initial state (okg_diag.cuh) -------------------------
@@ -1664,7 +1752,9 @@ static void build(okg_ctx* c) {
       const int ncv = (int)c->lv.back().g.N;
       for (size_t l = 1; l + 1 < c->lv.size(); ++l) {
         const Level& L = c->lv[l];
-        if (!(L.g.n <= tail_max_n<DIM>() && (int64_t)L.g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL &&
+        // (the kernel is instantiated for power-of-two first levels only)
+        const bool pow2 = L.g.n >= 2 && (L.g.n & (L.g.n - 1)) == 0;
+        if (!(pow2 && L.g.n <= tail_max_n<DIM>() && (int64_t)L.g.N <= tmax && c->lv.size() - l <= (size_t)TAIL_MAXL &&
               (S == 1 || (int)l >= c->L_rep)))
           continue;
         // cluster size: split the coarse inverse so each CTA stages <= 96 KB of it
@@ -1770,11 +1860,21 @@ static void build(okg_ctx* c) {
   c->vcap = cycle_len + 1;
   c->V = dalloc(c, (size_t)c->vcap * N2);
   for (double** b : {&c->gb, &c->gx, &c->gr, &c->pin, &c->pz, &c->pw, &c->gt}) *b = lvec(c, L0, 0, 2);
-  for (double** b : {&c->cd0, &c->cd1, &c->cr, &c->cr2, &c->r2p, &c->sy, &c->st, &c->kv, &c->zz, &c->rr, &c->z2,
+  for (double** b : {&c->cd0, &c->cd1, &c->cr, &c->cr2, &c->cad, &c->r2p, &c->sy, &c->st, &c->kv, &c->zz, &c->rr, &c->z2,
                      &c->shr, &c->u_old, &c->w_old, &c->u, &c->w})
     *b = lvec(c, L0, 0);
-  // Chebyshev bounds and coefficients
-  jacobi_spectrum<DIM>(c, c->lambda_lo, c->lambda_hi);
+  // Chebyshev bounds and coefficients (precond.hpp:156-166)
+  c->ssor = p.cheby_ssor != 0;
+  {
+    const int ncol = DIM == 3 ? c->fine.s * c->fine.s : c->fine.s;
+    c->ssor_cluster = std::min(8, (ncol + SSOR_NT - 1) / SSOR_NT);
+  }
+  if (c->ssor) {
+    if (c->nslabs > 1) THROW(OKG_ECONFIG, "config: cheby_precond = 'ssor' needs one slab (sequential sweeps)");
+    ssor_spectrum<DIM>(c, c->lambda_lo, c->lambda_hi);
+  } else {
+    jacobi_spectrum<DIM>(c, c->lambda_lo, c->lambda_hi);
+  }
   {
     const double lmin = c->lambda_lo, lmax = c->lambda_hi;
     if (lmin <= 0.0) THROW(OKG_EINVAL, "chebyshev: lambda_min must be positive");
@@ -1935,6 +2035,10 @@ static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double*
       note(c);
       break;
     case OKG_OP_COARSE_SOLVE: coarse_solve<DIM>(c, x, y); break;
+    case OKG_OP_SSOR_M:
+      if (c->nslabs > 1) THROW(OKG_EINVAL, "okg_apply: SSOR sweeps need one slab");
+      ssor_apply<DIM>(c, c->M, x, y, c->cr2);
+      break;
     default: THROW(OKG_EINVAL, "okg_apply: unknown kind %d", kind);
   }
 }
@@ -2634,7 +2738,7 @@ int okg_linearize_host(okg_ctx* c, const double* u) {
 
 int okg_apply_host(okg_ctx* c, int32_t kind, int32_t level, const double* x, double* y) {
   if (!c || !x || !y) return fail(OKG_EINVAL, "okg_apply_host: null argument");
-  if (kind < OKG_OP_M || kind > OKG_OP_COARSE_SOLVE) return fail(OKG_EINVAL, "okg_apply_host: unknown kind %d", kind);
+  if (kind < OKG_OP_M || kind > OKG_OP_SSOR_M) return fail(OKG_EINVAL, "okg_apply_host: unknown kind %d", kind);
   const bool level0 = !(kind == OKG_OP_PROLONG || kind == OKG_OP_RESTRICT || kind == OKG_OP_COARSE_SOLVE ||
                         (kind == OKG_OP_SHAT && level != 0));
   if (c->handle && !level0)

@@ -28,14 +28,15 @@ def load_golden(name):
 def golden_params(g, kind="port"):
     import pyoracle as po
     return po.baseline_params(int(g["dim"]), int(g["n"]), eps=float(g["eps"]), m=float(g["m"]),
-                              kind=kind, min_coarse_size=int(g["min_coarse"]))
+                              kind=kind, min_coarse_size=int(g["min_coarse"]), cheby_ssor=int(g.get("ssor", 0)))
 
 
 def golden_config(g):
     import paper_1603_04570_b200 as okg
     return okg.SolverConfig(dim=int(g["dim"]), n=int(g["n"]), eps=float(g["eps"]), m=float(g["m"]),
                             dt=float(g["eps"]) ** 2, sigma=100.0, theta=0.5, newton_tol=1e-8,
-                            gmres_tol=1e-10, gmres_restart=30, min_coarse_size=int(g["min_coarse"]))
+                            gmres_tol=1e-10, gmres_restart=30, min_coarse_size=int(g["min_coarse"]),
+                            cheby_precond="ssor" if int(g.get("ssor", 0)) else "jacobi")
 
 
 def relerr(a, b):

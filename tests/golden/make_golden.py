@@ -31,6 +31,10 @@ CASES = [
     ("d3n8mg", 3, 8, 0.0, 0.02, 4, 10),
     # non-default eps / mean
     ("d2n32e01", 2, 32, 0.1, 0.01, 1),
+    # cheby_precond = ssor (krylov.hpp:322-418)
+    ("d2n16ssor", 2, 16, 0.1, 0.02, 1, None, 1),
+    ("d3n8ssor", 3, 8, 0.0, 0.02, 2, None, 1),
+    ("d2n16mgssor", 2, 16, 0.0, 0.02, 3, 20, 1),
 ]
 
 OPS = [("M", po.M), ("K", po.K), ("A", po.A), ("VCYCLE", po.VCYCLE), ("SHAT_INV", po.SHAT_INV),
@@ -38,14 +42,15 @@ OPS = [("M", po.M), ("K", po.K), ("A", po.A), ("VCYCLE", po.VCYCLE), ("SHAT_INV"
        ("SCHUR_TILDE_INV", po.SCHUR_TILDE_INV), ("S_INV_APPROX", po.S_INV_APPROX)]
 
 
-def make(name, dim, n, m, eps, seed, min_coarse=None):
+def make(name, dim, n, m, eps, seed, min_coarse=None, ssor=0):
     kw = {} if min_coarse is None else {"min_coarse_size": min_coarse}
+    kw["cheby_ssor"] = ssor
     p = po.baseline_params(dim, n, eps=eps, m=m, kind="ref", **kw)
     o = po.Oracle(p, "ref")
     N = o.n
     rng = np.random.default_rng(1000 + dim * 100 + n)
     out = {"dim": dim, "n": n, "m": m, "eps": eps, "seed": seed, "N": N,
-           "min_coarse": p.min_coarse_size,
+           "min_coarse": p.min_coarse_size, "ssor": ssor,
            "levels": np.array([o.level_size(l) for l in range(o.levels)])}
     sc = o.scalars()
     out["scalars"] = np.array([sc[k] for k in ("c", "sqrt_c", "a_coeff", "dt_theta", "lambda_lo",

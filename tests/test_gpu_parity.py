@@ -375,3 +375,45 @@ def test_two_step_chebyshev_bit_identical(n, k):
         ctx.close()
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 16), (2, 48), (2, 64), (3, 8), (3, 16), (3, 24)])
+def test_ssor_sweeps_bit_exact(dim, n):
+    """okg_ssor.cuh: the hyperplane-wavefront SSOR sweeps reproduce the reference's
+    sequential SsorSweeps(M, 1).apply_inv bit for bit (power-of-two grids); the Lanczos bounds of
+    estimate_ssor_spectrum agree to rounding (dot-product order)."""
+    cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, cheby_precond="ssor")
+    ctx = okg.SchurContext(cfg)
+    o = po.Oracle(po.baseline_params(dim, n, kind="port", dt=4e-4, cheby_ssor=1), "port")
+    b = np.random.default_rng(n).uniform(-1, 1, ctx.n)
+    got, want = ctx.apply(_lib.OP_SSOR_M, b), o.apply(po.SSOR_M, b)
+    if n & (n - 1) == 0:  # power-of-two grid: the class tables are the reference's CSR rows exactly
+        assert np.array_equal(got, want)
+    else:  # the reference's element matrices carry coordinate rounding (i*h inexact)
+        assert relerr(got, want) <= 1e-13
+    sc = o.scalars()
+    assert abs(ctx.lambda_lo - sc["lambda_lo"]) <= 1e-12 * sc["lambda_lo"]
+    assert abs(ctx.lambda_hi - sc["lambda_hi"]) <= 1e-12 * sc["lambda_hi"]
+    ctx.close()
+
+
+def test_ssor_rejects_slabs():
+    cfg = okg.SolverConfig(dim=2, n=64, m=0.0, dt=4e-4, cheby_precond="ssor")
+    with pytest.raises(okg.ConfigError, match="ssor"):
+        okg.SchurContext(cfg, nslabs=2)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 48), (2, 50), (2, 100), (3, 24), (3, 40)])
+def test_non_power_of_two_grids(dim, n):
+    """eps-study meshes (n = round(2/eps): 50, 100, ...) and other n = 2^k * odd."""
+    cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30, max_dofs=10 ** 7)
+    ctx = okg.SchurContext(cfg)
+    st0 = okg.State(okg.seeded_ic(ctx.n, 1, 0.0), np.zeros(ctx.n))
+    ctx.set_state(st0)
+    s = ctx.step_resident()
+    o = po.Oracle(po.baseline_params(dim, n, kind="port", dt=4e-4), "port")
+    un, wn, ost = o.newton_solve(st0.u, st0.w)
+    assert s.converged and s.newton_iters == ost.newton_iters
+    assert all(abs(a - b) <= 1 for a, b in zip(s.gmres_iters, ost.gmres_iters))
+    assert relerr(ctx.get_state().u, un) <= 1e-8
+    ctx.close()
