@@ -40,9 +40,10 @@ __global__ void __launch_bounds__(TileCfg<2>::NT) k_cheb2(Grid g, Op<2> op, Tili
   constexpr int NO = Traits<2>::NOFF, TK = TileCfg<2>::TK, NT = TileCfg<2>::NT;
   const int tid = threadIdx.x;
   const int n = g.n;
-  if ((int)blockIdx.x >= tl.ncore) {
+  const int nbb = (int)((tl.nbnd + NT - 1) / NT);  // boundary CTAs first (see k_tiled)
+  if ((int)blockIdx.x < nbb) {
     // ---- boundary vertex: step a on its 1-ring, then step b ----
-    const uint32_t t = (blockIdx.x - tl.ncore) * NT + tid;
+    const uint32_t t = blockIdx.x * NT + tid;
     if (t >= tl.nbnd) return;
     const uint32_t idx = __ldg(tl.bnd + t);
     const int vi = (int)(idx / (uint32_t)g.s), vk = (int)(idx - (uint32_t)vi * g.s);
@@ -91,8 +92,9 @@ __global__ void __launch_bounds__(TileCfg<2>::NT) k_cheb2(Grid g, Op<2> op, Tili
   double* sd = sm;                        // d on rows i0-2 .. i0+ni+1, cols k0-2 .. k0+TK+1
   double* sr;                              // r, then r1, on the 1-ring region (right after d)
   double* s1;                              // d1 on the 1-ring region
-  const int kt = blockIdx.x % tl.ktiles;
-  const int ic = blockIdx.x / tl.ktiles;
+  const int cb = (int)blockIdx.x - nbb;
+  const int kt = cb % tl.ktiles;
+  const int ic = cb / tl.ktiles;
   const int k0 = 1 + kt * TK;
   const int i0 = tl.ci0 + ic * TI;
   const int ni = min(TI, tl.ci1 - i0);

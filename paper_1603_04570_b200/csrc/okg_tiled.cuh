@@ -161,9 +161,12 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
   using TC = TileCfg<DIM>;
   constexpr int NO = Traits<DIM>::NOFF;
   const int tid = threadIdx.x;
-  if ((int)blockIdx.x >= tl.ncore) {
+  // boundary CTAs come first: their gathers are the longest path of the kernel,
+  // so they should overlap the core tiles instead of forming its tail
+  const int nbb = (int)((tl.nbnd + TC::NT - 1) / TC::NT);
+  if ((int)blockIdx.x < nbb) {
     // ---- boundary vertices: class-table path ----
-    const uint32_t t = (blockIdx.x - tl.ncore) * TC::NT + tid;
+    const uint32_t t = blockIdx.x * TC::NT + tid;
     if (t >= tl.nbnd) return;
     const uint32_t idx = __ldg(tl.bnd + t);
     const Node<DIM> nd = locate<DIM>(g, idx);
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT) k_tiled(Grid g, Op<DIM> op, 
   }
   // ---- core tile ----
   extern __shared__ double tile[];
-  int b = blockIdx.x;
+  int b = (int)blockIdx.x - nbb;
   const int kt = b % tl.ktiles;
   b /= tl.ktiles;
   const int jt = DIM == 3 ? b % tl.jtiles : 0;

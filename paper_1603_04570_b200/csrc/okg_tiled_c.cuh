@@ -106,8 +106,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB_C) k_tile
   const int tid = threadIdx.x;
   double nrm[1] = {0.0};
   extern __shared__ double tile[];
-  if ((int)blockIdx.x >= tl.ncore) {
-    const uint32_t t = (blockIdx.x - tl.ncore) * TC::NT + tid;
+  const int nbb = (int)((tl.nbnd + TC::NT - 1) / TC::NT);  // boundary CTAs first (see k_tiled)
+  if ((int)blockIdx.x < nbb) {
+    const uint32_t t = blockIdx.x * TC::NT + tid;
     if (t < tl.nbnd) {
       const uint32_t idx = __ldg(tl.bnd + t);
       const Node<DIM> nd = locate<DIM>(g, idx);
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB_C) k_tile
       c_vertex<DIM, MODE>(g, Mop, Kop, Aop, a, idx, nd.cls, xs, vs, b1, b2, nrm[0]);
     }
   } else {
-    int bb = blockIdx.x;
+    int bb = (int)blockIdx.x - nbb;
     const int kt = bb % tl.ktiles;
     bb /= tl.ktiles;
     const int jt = DIM == 3 ? bb % tl.jtiles : 0;
