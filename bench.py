@@ -42,7 +42,19 @@ WORKLOADS = {
                   "eps=0.02 sigma=100 m=0 theta=0.5 dt=eps^2, seed 0, GMRES(30) rtol 1e-10, newton_tol 1e-8"),
     "c1_2d64": (2, 64, 0.02, 0.0, 0, 64,
                 "BASELINE configs[0]: 2D 64^2, seed 0"),
+    # configs[4]: 800^3 on 8 GPUs; one GPU runs the per-GPU share, 400^3 (64.5M vertices,
+    # 129M DoFs ~ 801^3 / 8), which coarsens to the same 26^3 = 17,576-unknown coarsest level
+    # as 800^3 (min_coarse_size raised to admit it, see MIN_COARSE)
+    "c5_3d800": (3, 800, 0.02, 0.0, 2, 32,
+                 "BASELINE configs[4]: 3D unit cube, 6 tets per cube, P1, eps=0.02 sigma=100 m=0 theta=0.5 "
+                 "dt=eps^2, seed 2, w0=0, GMRES(30) rtol 1e-10, newton_tol 1e-8, matrix-free; 800^3 "
+                 "(1.03B DoFs) on 8 GPUs, weak slices of ~64.5M vertices per GPU (1 GPU: 400^3, 129M DoFs); "
+                 "coarsest 26^3 = 17,576 (min_coarse_size 17576), dense inverse factorised on the device"),
 }
+
+# min_coarse_size per workload (default 500 = SolverConfig's): configs[4] needs the
+# reference's knob raised so its direct coarse solve admits 26^3 (multigrid.hpp:67-71)
+MIN_COARSE = {"c5_3d800": 17576}
 
 # N > 1 (torchrun, one process per GPU, one x-plane slab each): weak scaling keeps
 # the vertices per GPU about fixed with meshes whose hierarchy still coarsens to a
@@ -51,6 +63,7 @@ WEAK_N = {
     "c4_3d128": {1: 128, 2: 160, 4: 192, 8: 256},      # 2.15M, 2.09M, 1.80M, 2.12M vertices per GPU
     "c2_2d2048": {1: 2048, 2: 2944, 4: 4096, 8: 5888},  # 4.20M, 4.34M, 4.20M, 4.33M vertices per GPU
     "c1_2d64": {1: 64, 2: 96, 4: 128, 8: 192},
+    "c5_3d800": {1: 400, 2: 512, 4: 640, 8: 800},      # 64.5M, 67.4M, 65.8M, 64.2M vertices per GPU
 }
 
 # dominant kernel for the roofline object (top kernel by share of the step in
@@ -211,12 +224,13 @@ def main():
     import ctypes as C
 
     dim, n, eps, m, seed, n_cpu, desc = WORKLOADS[args.workload]
-    if world > 1 and args.scaling == "weak":
+    if (world > 1 and args.scaling == "weak") or (world == 1 and args.workload == "c5_3d800"):
         n = WEAK_N[args.workload].get(world)
         if n is None:
             raise SystemExit(f"--scaling weak: no mesh for {world} GPUs (have {sorted(WEAK_N[args.workload])})")
     cfg = okg.SolverConfig(dim=dim, n=n, eps=eps, m=m, sigma=100.0, theta=0.5, dt=eps * eps,
-                           newton_tol=1e-8, gmres_tol=1e-10, gmres_restart=30)
+                           newton_tol=1e-8, gmres_tol=1e-10, gmres_restart=30,
+                           min_coarse_size=MIN_COARSE.get(args.workload, 500))
     t0 = time.time()
     if world > 1:
         # one slab per process: rank 0 makes the NCCL id of the solver's own communicator
@@ -355,7 +369,7 @@ def main():
                        "parallelism": "1 GPU" if world == 1 else
                        (f"{world} x-plane slabs, one per GPU/process; ghost planes by NCCL send/recv, "
                         f"Krylov sums by NCCL allreduce; planes per rank {ctx.slab_planes}"),
-                       "l2": "per-step working set (1.1 GB Krylov basis) >> 126 MB L2; no flush",
+                       "l2": f"per-step working set ({31 * 2 * N * 8 / 1e9:.1f} GB Krylov basis) >> 126 MB L2; no flush",
                        "setup_s": setup_s, "levels": ctx.level_sizes},
             "newton_iters": [s.newton_iters for s in stats],
             "gmres_iters": [s.gmres_iters for s in stats],

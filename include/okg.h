@@ -83,6 +83,10 @@ typedef struct okg_params {
                                < 0 = one step per pass */
   int32_t cheby_ssor;       /* SolverConfig::cheby_precond: 0 = "jacobi", 1 = "ssor" (SSOR
                                sweeps as hyperplane wavefronts, one slab only) */
+  int32_t coarse_split;     /* coarsest level above 2000 unknowns (device-factorised inverse):
+                               0 = default (each slab multiplies the rows of its own coarse
+                               planes, then the planes are all-gathered), < 0 = every slab
+                               multiplies all rows */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */

@@ -77,7 +77,7 @@ class SolverConfig:
     def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
                   tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
                   mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
-                  tail_cluster: int = 0, cheb_fuse: int = 0) -> _lib.Params:
+                  tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -95,6 +95,7 @@ class SolverConfig:
         p.slab_devices = 1 if slab_devices else 0
         p.tail_cluster = tail_cluster
         p.cheb_fuse = cheb_fuse
+        p.coarse_split = coarse_split
         p.cheby_ssor = 1 if self.cheby_precond == "ssor" else 0
         return p
 
@@ -264,12 +265,26 @@ class DeviceArray:
         check(lib.okg_memcpy_h2d(d.ptr, a.ctypes.data_as(C.c_void_p), a.size * 8))
         return d
 
+    @classmethod
+    def view(cls, base: "DeviceArray", offset: int, n: int) -> "DeviceArray":
+        """Non-owning view of base[offset : offset + n] (offset in doubles)."""
+        if offset < 0 or offset + n > base.n:
+            raise ValueError("DeviceArray.view: out of range")
+        d = cls.__new__(cls)
+        d.n = int(n)
+        d.ptr = C.c_void_p(base.ptr.value + 8 * int(offset))
+        d.base = base
+        return d
+
     def numpy(self) -> np.ndarray:
         out = np.empty(self.n)
         check(lib.okg_memcpy_d2h(out.ctypes.data_as(C.c_void_p), self.ptr, self.n * 8))
         return out
 
     def free(self):
+        if getattr(self, "base", None) is not None:  # a view owns nothing
+            self.ptr = C.c_void_p()
+            return
         if self.ptr:
             lib.okg_device_free(self.ptr)
             self.ptr = C.c_void_p()
@@ -289,7 +304,7 @@ class SchurContext:
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
                  pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
                  rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None,
-                 tail_cluster: int = 0, cheb_fuse: int = 0):
+                 tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0):
         """nslabs > 1: x-plane slab decomposition, one host thread + stream per
         slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
         `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
@@ -299,7 +314,7 @@ class SchurContext:
         self.device = device
         self.handle = C.c_void_p()
         params = cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl, mg_fuse,
-                               nslabs, slab_devices, tail_cluster, cheb_fuse)
+                               nslabs, slab_devices, tail_cluster, cheb_fuse, coarse_split)
         if rank is None:
             check(lib.okg_create(C.byref(params), C.byref(self.handle)))
         else:

@@ -47,6 +47,7 @@ class Params(C.Structure):
         ("mg_fuse", C.c_int32), ("nslabs", C.c_int32), ("slab_devices", C.c_int32),
         ("tail_cluster", C.c_int32), ("cheb_fuse", C.c_int32),
         ("cheby_ssor", C.c_int32),
+        ("coarse_split", C.c_int32),
     ]
 
 

@@ -37,6 +37,7 @@
 #include "okg_cheb2.cuh"
 #include "okg_ssor.cuh"
 #include "okg_nccl.h"
+#include "okg_cusolver.h"
 #include "okg_tables.h"
 
 namespace okg {
@@ -124,6 +125,11 @@ struct okg_ctx {
   std::vector<Level> lv;
   int nc = 0;
   double* Ainv = nullptr;
+  // large coarsest level (nc > 2000): device-factorised inverse, rows [coarse_r0, coarse_r1)
+  // of it on this slab (all rows unless the level is split for the solve), row stride coarse_ld
+  bool coarse_big = false, coarse_split = false;
+  int coarse_r0 = 0, coarse_r1 = 0;
+  size_t coarse_ld = 0;
   int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
   int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
   double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
@@ -631,10 +637,92 @@ static void copy(okg_ctx* c, const double* x, double* y, size_t n) {
 }
 
 // ---- multigrid (multigrid.hpp:97-149) --------------------------------------
+static void allgather_planes(okg_ctx* c, int l, double* x);
+
 template <int DIM>
 static void coarse_solve(okg_ctx* c, const double* b, double* y) {
-  launch(c, k_coarse_solve, (c->nc + BS / 32 - 1) / (BS / 32), BS, 0, c->nc, c->Ainv, b, y);
+  if (!c->coarse_big) {
+    launch(c, k_coarse_solve, (c->nc + BS / 32 - 1) / (BS / 32), BS, 0, c->nc, c->Ainv, b, y);
+    note(c);
+    return;
+  }
+  // large coarsest level: this slab's rows of the inverse, then (split) the planes of
+  // every slab's rows are all-gathered -- the same ranges the restriction gathers
+  Level& L = c->lv.back();
+  const int last = (int)c->lv.size() - 1;
+  if (reinterpret_cast<uintptr_t>(b) % 16 != 0) {
+    copy(c, b, L.eb, (size_t)c->nc);
+    b = L.eb;
+  }
+  double* tgt = c->coarse_split ? L.ea : y;
+  const int rows = c->coarse_r1 - c->coarse_r0;
+  launch(c, k_coarse_gemv, (rows + BS / 32 - 1) / (BS / 32), BS, 0, c->nc, c->coarse_r0, c->coarse_r1, c->coarse_ld,
+         (const double*)c->Ainv, b, tgt);
   note(c);
+  if (c->coarse_split) {
+    allgather_planes(c, last, L.ea);
+    if (y != L.ea) copy(c, L.ea, y, (size_t)c->nc);
+  }
+}
+
+// Setup of the large coarsest level (nc > 2000): Cholesky + inverse of the dense
+// operator on the device (cuSOLVER potrf/potri, okg_cusolver.h), then rows
+// [r0, r1) are written in full (stride ld) to c->Ainv.  The host path
+// (dense_spd_inverse) is O(nc^3) on one core: hours at 26^3 = 17,576.
+static void coarse_inverse_device(okg_ctx* c, const std::vector<double>& Ad, int nc, int r0, int r1) {
+  std::string why;
+  const CusolverApi* cs = cusolver_api(&why);
+  if (!cs) THROW(OKG_ECUDA, "coarse solve (%d unknowns > 2000): %s", nc, why.c_str());
+  const size_t nn = (size_t)nc * nc;
+  double* F = nullptr;
+  int* info = nullptr;
+  double* work = nullptr;
+  cusolverDnHandle_t h = nullptr;
+  auto cleanup = [&]() {
+    if (h) cs->Destroy(h);
+    cudaFree(F);
+    cudaFree(info);
+    cudaFree(work);
+  };
+  try {
+    cudaError_t e = cudaMalloc(&F, nn * sizeof(double));
+    if (e != cudaSuccess) THROW(OKG_ENOMEM, "cudaMalloc(%zu bytes) for the coarse factor: %s", nn * sizeof(double),
+                                cudaGetErrorString(e));
+    CK(cudaMalloc(&info, sizeof(int)));
+    CK(cudaMemcpyAsync(F, Ad.data(), nn * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (cs->Create(&h) != CUSOLVER_STATUS_SUCCESS) THROW(OKG_ECUDA, "cusolverDnCreate failed");
+    cs->SetStream(h, c->stream);
+    int lw1 = 0, lw2 = 0;
+    if (cs->PotrfBufferSize(h, CUBLAS_FILL_MODE_LOWER, nc, F, nc, &lw1) != CUSOLVER_STATUS_SUCCESS ||
+        cs->PotriBufferSize(h, CUBLAS_FILL_MODE_LOWER, nc, F, nc, &lw2) != CUSOLVER_STATUS_SUCCESS)
+      THROW(OKG_ECUDA, "cusolverDn potrf/potri bufferSize failed");
+    const int lw = std::max(std::max(lw1, lw2), 1);
+    CK(cudaMalloc(&work, (size_t)lw * sizeof(double)));
+    int hinfo = 0;
+    if (cs->Potrf(h, CUBLAS_FILL_MODE_LOWER, nc, F, nc, work, lw, info) != CUSOLVER_STATUS_SUCCESS)
+      THROW(OKG_ECUDA, "cusolverDnDpotrf failed");
+    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (hinfo != 0) THROW(OKG_ENUMERICAL, "Cholesky: matrix not positive definite");
+    if (cs->Potri(h, CUBLAS_FILL_MODE_LOWER, nc, F, nc, work, lw, info) != CUSOLVER_STATUS_SUCCESS)
+      THROW(OKG_ECUDA, "cusolverDnDpotri failed");
+    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (hinfo != 0) THROW(OKG_ENUMERICAL, "Cholesky: inverse failed (info %d)", hinfo);
+    const size_t ld = (size_t)(nc + 1) & ~(size_t)1;
+    c->Ainv = dalloc(c, (size_t)(r1 - r0) * ld);
+    k_coarse_rows<<<148 * 8, 256, 0, c->stream>>>(nc, r0, r1, ld, F, c->Ainv);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    c->coarse_ld = ld;
+    c->coarse_r0 = r0;
+    c->coarse_r1 = r1;
+    c->coarse_big = true;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
 }
 
 // levels tail_start..coarsest in one launch (okg_tail.cuh)
@@ -1835,10 +1923,22 @@ static void build(okg_ctx* c) {
         Ad[static_cast<size_t>(i) * nc + j] = Lc.shat.htab[static_cast<size_t>(cls) * (NO + 1) + o];
       }
     }
-    if (!dense_spd_inverse(Ad, nc, Ai)) THROW(OKG_ENUMERICAL, "Cholesky: matrix not positive definite");
     c->nc = nc;
-    c->Ainv = dalloc(c, Ai.size());
-    CK(cudaMemcpyAsync(c->Ainv, Ai.data(), Ai.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (nc <= 2000) {
+      if (!dense_spd_inverse(Ad, nc, Ai)) THROW(OKG_ENUMERICAL, "Cholesky: matrix not positive definite");
+      c->Ainv = dalloc(c, Ai.size());
+      CK(cudaMemcpyAsync(c->Ainv, Ai.data(), Ai.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    } else {
+      // split the rows over the slabs when the coarsest is the first replicated level
+      // (its planes are then gathered with the restriction's ranges, allgather_planes)
+      int r0 = 0, r1 = nc;
+      c->coarse_split = S > 1 && c->L_rep == (int)c->lv.size() - 1 && p.coarse_split >= 0;
+      if (c->coarse_split) {
+        r0 = c->rep_lo[c->rank] * (int)Lc.g.ps;
+        r1 = c->rep_hi[c->rank] * (int)Lc.g.ps;
+      }
+      coarse_inverse_device(c, Ad, nc, r0, r1);
+    }
   }
   // buffers
   const size_t N2 = c->N2;

@@ -263,6 +263,61 @@ __global__ void __launch_bounds__(BS) k_coarse_solve(int nc, const double* __res
   if (lane == 0) y[row] = s;
 }
 
+// Large coarsest level (nc > 2000, e.g. 26^3 = 17,576 for 400^3 / 800^3): rows
+// [r0, r1) of the explicit inverse, row stride ld (even, so rows are 16-byte
+// aligned), b 16-byte aligned.  One warp per row; 2 x 16-byte loads of the row
+// and of b per lane and step, 4 steps in flight: the inverse (2.47 GB at
+// 17,576) streams from HBM at the copy rate while b stays in L1/L2.
+__global__ void __launch_bounds__(BS) k_coarse_gemv(int nc, int r0, int r1, size_t ld,
+                                                    const double* __restrict__ Ainv,
+                                                    const double* __restrict__ b, double* __restrict__ y) {
+  PDL_ENTRY();
+  const int row = r0 + blockIdx.x * (BS / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= r1) return;
+  const double2* a2 = reinterpret_cast<const double2*>(Ainv + (size_t)(row - r0) * ld);
+  const double2* b2 = reinterpret_cast<const double2*>(b);
+  const int n2 = nc >> 1;
+  double s0 = 0.0, s1 = 0.0;
+  int j = lane;
+  for (; j + 96 < n2; j += 128) {
+    double2 a[4], v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] = __ldcs(a2 + j + 32 * q);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldg(b2 + j + 32 * q);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s0 = fma(a[q].x, v[q].x, s0);
+      s1 = fma(a[q].y, v[q].y, s1);
+    }
+  }
+  for (; j < n2; j += 32) {
+    const double2 a = __ldcs(a2 + j), v = __ldg(b2 + j);
+    s0 = fma(a.x, v.x, s0);
+    s1 = fma(a.y, v.y, s1);
+  }
+  double s = s0 + s1;
+  if ((nc & 1) && lane == 0) s = fma(Ainv[(size_t)(row - r0) * ld + nc - 1], b[nc - 1], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = s;
+}
+
+// Setup of the large coarse inverse: cuSOLVER potri leaves A^{-1} in the
+// column-major lower triangle = the row-major upper triangle (j >= i) of F;
+// write rows [r0, r1) in full with row stride ld (padding zero).
+__global__ void k_coarse_rows(int nc, int r0, int r1, size_t ld, const double* __restrict__ F,
+                              double* __restrict__ out) {
+  const size_t total = (size_t)(r1 - r0) * ld;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int i = r0 + (int)(t / ld), j = (int)(t % ld);
+    double v = 0.0;
+    if (j < nc) v = j >= i ? F[(size_t)i * nc + j] : F[(size_t)j * nc + i];
+    out[t] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Chebyshev semi-iteration with Jacobi preconditioning (krylov.hpp:158-202).
 //   first:  d0 = (r0 * D^-1) * (1/theta)                 x1 = d0 (implicit)

@@ -35,6 +35,10 @@ CASES = [
     ("d2n16ssor", 2, 16, 0.1, 0.02, 1, None, 1),
     ("d3n8ssor", 3, 8, 0.0, 0.02, 2, None, 1),
     ("d2n16mgssor", 2, 16, 0.0, 0.02, 3, 20, 1),
+    # coarsest level above the 2000-unknown dense default (46^2 = 2116, min_coarse_size
+    # raised so the reference admits it, multigrid.hpp:67-71): the device-factorised
+    # coarse inverse of the 400^3 / 800^3 hierarchies (26^3 = 17,576)
+    ("d2n90big", 2, 90, 0.0, 0.02, 5, 2116),
 ]
 
 OPS = [("M", po.M), ("K", po.K), ("A", po.A), ("VCYCLE", po.VCYCLE), ("SHAT_INV", po.SHAT_INV),
@@ -119,8 +123,12 @@ def make(name, dim, n, m, eps, seed, min_coarse=None, ssor=0):
 if __name__ == "__main__":
     if not po.available("ref"):
         sys.exit("oracle/_ref/libokref.so missing: run `make -C oracle ref` where /root/reference exists")
+    only = sys.argv[1:]
     for case in CASES:
-        make(*case)
+        if not only or case[0] in only:
+            make(*case)
+    if only:
+        sys.exit(0)
     # KAT: 64-grid hierarchy with min_coarse_size=100 (test_multigrid.cpp:34-44)
     o = po.Oracle(po.baseline_params(2, 64, kind="ref", min_coarse_size=100), "ref")
     np.savez_compressed(os.path.join(HERE, "hierarchy64.npz"),
