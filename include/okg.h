@@ -130,6 +130,7 @@ typedef struct okg_info {
   int32_t rep_level;          /* first level replicated on every slab (levels if none) */
   int32_t slab_ilo[16], slab_ihi[16]; /* owned x-planes [ilo, ihi) of the finest level per slab */
   int32_t tail_cluster;       /* CTAs in the tail's thread-block cluster */
+  int32_t coarse_rows;        /* rows of the coarse inverse this slab multiplies */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */

@@ -341,6 +341,7 @@ class SchurContext:
         self.tail_start = int(info.tail_start)
         self.tail_cluster = int(info.tail_cluster)
         self.tiled_levels = [l for l in range(self.levels) if (info.tiled_mask >> l) & 1]
+        self.coarse_rows = int(info.coarse_rows)
         self.nslabs = int(info.nslabs)
         self.rep_level = int(info.rep_level)
         self.slab_planes = [(int(info.slab_ilo[r]), int(info.slab_ihi[r])) for r in range(self.nslabs)]

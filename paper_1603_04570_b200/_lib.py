@@ -78,6 +78,7 @@ class Info(C.Structure):
         ("tail_start", C.c_int32), ("tiled_mask", C.c_int32),
         ("nslabs", C.c_int32), ("rep_level", C.c_int32),
         ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16), ("tail_cluster", C.c_int32),
+        ("coarse_rows", C.c_int32),
     ]
 
 

@@ -79,6 +79,9 @@ def test_slabs_split_coarse_rows(dim, n, mcs, S, split):
     one = okg.SchurContext(cfg)
     many = okg.SchurContext(cfg, nslabs=S, coarse_split=split)
     assert many.rep_level == many.levels - 1  # the coarsest is the first replicated level
+    nc = one.level_sizes[-1]
+    assert one.coarse_rows == nc
+    assert (many.coarse_rows < nc) if split == 0 else (many.coarse_rows == nc)
     rng = np.random.default_rng(S)
     x = rng.standard_normal(one.n)
     u = okg.seeded_ic(one.n, 3, 0.1)

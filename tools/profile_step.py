@@ -13,7 +13,8 @@ from paper_1603_04570_b200 import _lib  # noqa: E402
 dim, n = int(sys.argv[1]), int(sys.argv[2])
 k = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 seed = int(sys.argv[4]) if len(sys.argv) > 4 else (2 if dim == 3 else 0)
-cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30)
+cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30,
+                       min_coarse_size=int(os.environ.get("OKG_MIN_COARSE", "500")))
 ctx = okg.SchurContext(cfg, tiled_min_n=int(os.environ.get("OKG_TILED", "0")),
                        tail_max_vertices=int(os.environ.get("OKG_TAIL", "0")),
                        pdl=os.environ.get("OKG_PDL", "1") == "1",

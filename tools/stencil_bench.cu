@@ -607,7 +607,11 @@ int run(int n, bool extras) {
   return 0;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    for (int a = 1; a < argc; ++a) run(atoi(argv[a]), false);
+    return 0;
+  }
   run(128, true);
   run(256, false);
   return 0;
