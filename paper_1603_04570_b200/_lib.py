@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libokg.so")
+LIB_PATH = os.environ.get("OKG_LIB") or os.path.join(HERE, "libokg.so")  # OKG_LIB: A/B builds (tools)
 
 OKG_OK = 0
 OKG_EINVAL = -1

@@ -569,13 +569,7 @@ static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& 
     CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributePreferredSharedMemoryCarveout, SMEM_CARVEOUT));
     attr = true;
   }
-  Tiling tt = L.tl;
-  unsigned blocks = L.tl_blocks;
-  if (getenv("OKG_DBG_NOBND")) {  // TEMP experiment: skip the boundary CTAs
-    blocks -= (tt.nbnd + TileCfg<DIM>::NT - 1) / TileCfg<DIM>::NT;
-    tt.nbnd = 0;
-  }
-  launch(c, k_tiled<DIM, LOAD, EPI, TI>, blocks, TileCfg<DIM>::NT, smem, L.g, dev_op<DIM>(op), tt, a);
+  launch(c, k_tiled<DIM, LOAD, EPI, TI>, L.tl_blocks, TileCfg<DIM>::NT, smem, L.g, dev_op<DIM>(op), L.tl, a);
   note(c);
 }
 

@@ -277,26 +277,37 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   }
   // stage planes i0-1 .. i0+ni: every element by cp.async (LDGSTS, zero-fill outside
   // the box), all in flight at once together with the pointwise prefetch above --
-  // no register staging (measured at 400^3: 1.6x the register-batched loop)
-  const int total = (ni + 2) * TC::PSZ;
-  for (int e = tid; e < total; e += TC::NT) {
-    const int p = e / TC::PSZ;
-    const int r = e - p * TC::PSZ;
+  // no register staging (measured at 400^3: 1.6x the register-batched loop).  The
+  // transform below visits in-plane element r = tid + q NT of every plane (offsets
+  // computed once, no per-element division).
+  constexpr int PER = (TC::PSZ + TC::NT - 1) / TC::NT;
+  int qoff[PER], qgj[PER], qgk[PER];
+  bool qin[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int r = tid + q * TC::NT;
     const int hj = DIM == 3 ? r / TC::PW : 0;
     const int hk = DIM == 3 ? r - hj * TC::PW : r;
-    const int gj = DIM == 3 ? j0 - 1 + hj : 0;
-    const int gk = k0 - 1 + hk;
-    const int ip = i0 - 1 + p;
-    const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
-    cp_async8(tile + e, a.x + lin, gk <= g.n && gj <= g.n);
+    qgj[q] = DIM == 3 ? j0 - 1 + hj : 0;
+    qgk[q] = k0 - 1 + hk;
+    qin[q] = r < TC::PSZ && qgk[q] <= g.n && qgj[q] <= g.n;
+    qoff[q] = DIM == 3 ? qgj[q] * g.s + qgk[q] : qgk[q];
   }
-  cp_commit();
-  cp_wait<0>();
-  if (LOAD != L_PLAIN) {
-    if (CSTAGE) __syncthreads();  // the coarse tile (other threads' copies) is visible
-    // staging transform of this thread's own elements (its copies have landed):
-    //   L_JAC0 r -> (w D^-1) r ; L_PROLONG e -> e + P e_c  (x + t, multigrid.hpp:111-112)
-    constexpr int CSI = CT::CJ * CT::CK, CSJ = CT::CK;
+  // issue order (measured, A/B on one box): per plane for the transformed loads and the
+  // Chebyshev step, in linear tile order for the plain sweeps (5 % either way)
+  constexpr bool PLANE_ISSUE = LOAD != L_PLAIN || EPI == T_CHEB;
+  if (PLANE_ISSUE) {
+#pragma unroll
+    for (int p = 0; p < TI + 2; ++p) {
+      if (p < ni + 2) {
+        const uint32_t pb0 = (uint32_t)(i0 - 1 + p) * pstride;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (tid + q * TC::NT < TC::PSZ) cp_async8(tile + p * TC::PSZ + tid + q * TC::NT, a.x + pb0 + qoff[q], qin[q]);
+      }
+    }
+  } else {
+    const int total = (ni + 2) * TC::PSZ;
     for (int e = tid; e < total; e += TC::NT) {
       const int p = e / TC::PSZ;
       const int r = e - p * TC::PSZ;
@@ -304,21 +315,49 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       const int hk = DIM == 3 ? r - hj * TC::PW : r;
       const int gj = DIM == 3 ? j0 - 1 + hj : 0;
       const int gk = k0 - 1 + hk;
+      const uint32_t lin = (uint32_t)(i0 - 1 + p) * pstride + (DIM == 3 ? (uint32_t)gj * g.s : 0u) + gk;
+      cp_async8(tile + e, a.x + lin, gk <= g.n && gj <= g.n);
+    }
+  }
+  cp_commit();
+  cp_wait<0>();
+  if (LOAD != L_PLAIN) {
+    __syncthreads();  // every copy (and the coarse tile) is visible
+    // staging transform:  L_JAC0 r -> (w D^-1) r ;
+    //                     L_PROLONG e -> e + P e_c  (x + t, multigrid.hpp:111-112)
+    constexpr int CSI = CT::CJ * CT::CK, CSJ = CT::CK;
+    // JAC0 on a tile whose halo holds no boundary vertex: one constant scale
+    const bool inner = i0 - 1 >= 1 && i0 + ni <= g.n - 1 && k0 - 1 >= 1 && k0 + TC::TK <= g.n - 1 &&
+                       (DIM == 2 || (j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1));
+    const double wd = a.omega * op.invd;
+#pragma unroll
+    for (int p = 0; p < TI + 2; ++p) {
+      if (p >= ni + 2) continue;
       const int ip = i0 - 1 + p;
-      if (gk > g.n || gj > g.n) continue;
-      if (LOAD == L_JAC0) {
-        const int cls = class_of<DIM>(g, ip, gj, gk);
-        const double invd =
-            cls == Traits<DIM>::INTERIOR ? op.invd : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
-        tile[e] = a.omega * invd * tile[e];
-      } else if (CSTAGE) {
-        const int li = (ip >> 1) - cbi, lj = DIM == 3 ? (gj >> 1) - cbj : 0, lk = (gk >> 1) - cbk;
-        const int hi = ((ip + 1) >> 1) - cbi, hj2 = DIM == 3 ? ((gj + 1) >> 1) - cbj : 0, hk2 = ((gk + 1) >> 1) - cbk;
-        const int lo = li * CSI + lj * CSJ + lk, up = hi * CSI + hj2 * CSJ + hk2;
-        const double t = lo == up ? ct[lo] : fma(0.5, ct[up], 0.5 * ct[lo]);
-        tile[e] = tile[e] + t;
-      } else {
-        tile[e] = tile[e] + prolong_at<DIM>(a.gc, a.x2, ip, gj, gk);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        if (!qin[q]) continue;
+        double& v = tile[p * TC::PSZ + tid + q * TC::NT];
+        if (LOAD == L_JAC0) {
+          if (inner) {
+            v = wd * v;
+          } else {
+            const int cls = class_of<DIM>(g, ip, qgj[q], qgk[q]);
+            const double invd = cls == Traits<DIM>::INTERIOR
+                                    ? op.invd
+                                    : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+            v = a.omega * invd * v;
+          }
+        } else if (CSTAGE) {
+          const int gj = qgj[q], gk = qgk[q];
+          const int lo = ((ip >> 1) - cbi) * CSI + (DIM == 3 ? ((gj >> 1) - cbj) * CSJ : 0) + ((gk >> 1) - cbk);
+          const int up = (((ip + 1) >> 1) - cbi) * CSI + (DIM == 3 ? (((gj + 1) >> 1) - cbj) * CSJ : 0) +
+                         (((gk + 1) >> 1) - cbk);
+          const double t = lo == up ? ct[lo] : fma(0.5, ct[up], 0.5 * ct[lo]);
+          v = v + t;
+        } else {
+          v = v + prolong_at<DIM>(a.gc, a.x2, ip, qgj[q], qgk[q]);
+        }
       }
     }
   }

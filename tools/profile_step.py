@@ -25,7 +25,20 @@ print(f"levels={ctx.level_sizes} tiled={ctx.tiled_levels} tail_start={ctx.tail_s
 ctx.set_state(okg.State(okg.seeded_ic(ctx.n, seed, 0.0), np.zeros(ctx.n)))
 setup = _lib.lib.okg_kernel_launch_count()
 print(f"setup_launches={setup}", flush=True)
+# ncu --profile-from-start off: only the timesteps are profiled (setup also runs
+# library kernels, e.g. the cuSOLVER factorisation of a large coarsest level)
+import ctypes  # noqa: E402
+try:
+    _rt = ctypes.CDLL("libcudart.so.12")
+except OSError:
+    _rt = None
+_lib.check(_lib.lib.okg_device_synchronize())
+if _rt is not None:
+    _rt.cudaProfilerStart()
 for i in range(k):
     st = ctx.step_resident()
     print(f"step {i}: newton={st.newton_iters} gmres={st.gmres_iters} t={st.seconds*1e3:.2f}ms "
           f"launches={st.kernel_launches}", flush=True)
+if _rt is not None:
+    _lib.check(_lib.lib.okg_device_synchronize())
+    _rt.cudaProfilerStop()
