@@ -132,6 +132,8 @@ struct okg_ctx {
   bool coarse_big = false, coarse_split = false;
   int coarse_r0 = 0, coarse_r1 = 0;
   size_t coarse_ld = 0;
+  int coarse_nb = 0;  // > 0: one slab, symmetric packed blocks (k_coarse_sym)
+  double *coarse_R = nullptr, *coarse_C = nullptr;
   int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
   int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
   double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
@@ -667,6 +669,16 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
     copy(c, b, L.eb, (size_t)c->nc);
     b = L.eb;
   }
+  if (c->coarse_nb > 0) {  // one slab: half the bytes through the symmetric block triangle
+    const int nb = c->coarse_nb;
+    launch(c, k_coarse_sym, (unsigned)(nb * (nb + 1) / 2), 256, 0, c->nc, (const double*)c->Ainv, b, c->coarse_R,
+           c->coarse_C);
+    note(c);
+    launch(c, k_coarse_sym_sum, (unsigned)nb, CB, 0, c->nc, nb, (const double*)c->coarse_R,
+           (const double*)c->coarse_C, y);
+    note(c);
+    return;
+  }
   double* tgt = c->coarse_split ? L.ea : y;
   const int rows = c->coarse_r1 - c->coarse_r0;
   launch(c, k_coarse_gemv, (rows + BS / 32 - 1) / (BS / 32), BS, 0, c->nc, c->coarse_r0, c->coarse_r1, c->coarse_ld,
@@ -723,8 +735,19 @@ static void coarse_inverse_device(okg_ctx* c, const std::vector<double>& Ad, int
     CK(cudaStreamSynchronize(c->stream));
     if (hinfo != 0) THROW(OKG_ENUMERICAL, "Cholesky: inverse failed (info %d)", hinfo);
     const size_t ld = (size_t)(nc + 1) & ~(size_t)1;
-    c->Ainv = dalloc(c, (size_t)(r1 - r0) * ld);
-    k_coarse_rows<<<148 * 8, 256, 0, c->stream>>>(nc, r0, r1, ld, F, c->Ainv);
+    if (r0 == 0 && r1 == nc && c->p.coarse_split >= 0) {
+      // all rows on this slab: symmetric packed blocks
+      const int nb = (nc + CB - 1) / CB;
+      const size_t nblk = (size_t)nb * (nb + 1) / 2;
+      c->Ainv = dalloc(c, nblk * CB * CB);
+      c->coarse_R = dalloc(c, nblk * CB);
+      c->coarse_C = dalloc(c, nblk * CB);
+      k_coarse_pack<<<148 * 8, 256, 0, c->stream>>>(nc, nb, F, c->Ainv);
+      c->coarse_nb = nb;
+    } else {
+      c->Ainv = dalloc(c, (size_t)(r1 - r0) * ld);
+      k_coarse_rows<<<148 * 8, 256, 0, c->stream>>>(nc, r0, r1, ld, F, c->Ainv);
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     c->coarse_ld = ld;

@@ -318,6 +318,93 @@ __global__ void k_coarse_rows(int nc, int r0, int r1, size_t ld, const double* _
   }
 }
 
+// Large coarsest level on one slab: the SYMMETRIC inverse stored as its lower block
+// triangle of CB x CB blocks (block (I, J), J <= I, row-major, packed index
+// I(I+1)/2 + J) -- half the bytes of the full matrix.  A CTA streams one block once
+// and produces both of its products: R = A_IJ x_J (rows of block I) and, off the
+// diagonal, C = A_IJ^T x_I (rows of block J); k_coarse_sym_sum adds the partials of
+// every row in a fixed order (deterministic, no atomics).
+constexpr int CB = 64;
+
+__device__ __forceinline__ void tri_index(int b, int& I, int& J) {
+  int i = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= b) ++i;
+  while (i * (i + 1) / 2 > b) --i;
+  I = i;
+  J = b - i * (i + 1) / 2;
+}
+
+__global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __restrict__ Ap,
+                                                    const double* __restrict__ x, double* __restrict__ R,
+                                                    double* __restrict__ Cp) {
+  PDL_ENTRY();
+  __shared__ double xs_i[CB], xs_j[CB];
+  __shared__ double cpart[8][CB];
+  int I, J;
+  tri_index(blockIdx.x, I, J);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid < CB) {
+    const int r = I * CB + tid, c = J * CB + tid;
+    xs_i[tid] = r < nc ? x[r] : 0.0;
+    xs_j[tid] = c < nc ? x[c] : 0.0;
+  }
+  const double2* blk = reinterpret_cast<const double2*>(Ap + (size_t)blockIdx.x * CB * CB);
+  double2 a[CB / 8];
+#pragma unroll
+  for (int q = 0; q < CB / 8; ++q) a[q] = __ldcs(blk + (size_t)(w + 8 * q) * (CB / 2) + lane);
+  __syncthreads();
+  const double xj0 = xs_j[2 * lane], xj1 = xs_j[2 * lane + 1];
+  double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < CB / 8; ++q) {
+    const int r = w + 8 * q;
+    double s = fma(a[q].y, xj1, a[q].x * xj0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) R[(size_t)blockIdx.x * CB + r] = s;
+    const double xr = xs_i[r];
+    c0 = fma(a[q].x, xr, c0);
+    c1 = fma(a[q].y, xr, c1);
+  }
+  if (I == J) return;
+  cpart[w][2 * lane] = c0;
+  cpart[w][2 * lane + 1] = c1;
+  __syncthreads();
+  if (tid < CB) {
+    double c = cpart[0][tid];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) c += cpart[q][tid];
+    Cp[(size_t)blockIdx.x * CB + tid] = c;
+  }
+}
+
+// y_r (r in block I) = sum_{J <= I} R(I,J)_r + sum_{K > I} C(K,I)_r
+__global__ void __launch_bounds__(CB) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
+                                                      const double* __restrict__ Cp, double* __restrict__ y) {
+  PDL_ENTRY();
+  const int I = blockIdx.x, t = threadIdx.x, r = I * CB + t;
+  double s = 0.0;
+  const size_t base = (size_t)I * (I + 1) / 2;
+  for (int J = 0; J <= I; ++J) s += R[(base + J) * CB + t];
+  for (int K = I + 1; K < nb; ++K) s += Cp[((size_t)K * (K + 1) / 2 + I) * CB + t];
+  if (r < nc) y[r] = s;
+}
+
+// setup: pack the lower block triangle of the full symmetric inverse (row-major upper
+// triangle of F valid, see k_coarse_rows), zero padding
+__global__ void k_coarse_pack(int nc, int nb, const double* __restrict__ F, double* __restrict__ Ap) {
+  const size_t total = (size_t)nb * (nb + 1) / 2 * CB * CB;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    int I, J;
+    tri_index((int)(t / (CB * CB)), I, J);
+    const int e = (int)(t % (CB * CB));
+    const int i = I * CB + e / CB, j = J * CB + e % CB;
+    double v = 0.0;
+    if (i < nc && j < nc) v = j >= i ? F[(size_t)i * nc + j] : F[(size_t)j * nc + i];
+    Ap[t] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Chebyshev semi-iteration with Jacobi preconditioning (krylov.hpp:158-202).
 //   first:  d0 = (r0 * D^-1) * (1/theta)                 x1 = d0 (implicit)

@@ -76,7 +76,7 @@ def test_misaligned_rhs_and_rerun_bit_identical():
 @pytest.mark.parametrize("split", [0, -1])
 def test_slabs_split_coarse_rows(dim, n, mcs, S, split):
     cfg = cfg_for(dim, n, mcs)
-    one = okg.SchurContext(cfg)
+    one = okg.SchurContext(cfg, coarse_split=-1)  # full rows (one slab would pack the symmetric blocks)
     many = okg.SchurContext(cfg, nslabs=S, coarse_split=split)
     assert many.rep_level == many.levels - 1  # the coarsest is the first replicated level
     nc = one.level_sizes[-1]
@@ -97,3 +97,23 @@ def test_slabs_split_coarse_rows(dim, n, mcs, S, split):
     assert relerr(sts[1][0].u, sts[0][0].u) <= 1e-10
     many.close()
     one.close()
+
+
+@pytest.mark.parametrize("dim,n,mcs", [(2, 90, 2116), (3, 30, 4096)])
+def test_symmetric_blocks_match_full_rows(dim, n, mcs):
+    # one slab: the inverse is stored as its lower block triangle (half the bytes) and
+    # both block products are formed from one read; the sums run in another order than
+    # the full-row kernel's, so the two agree to rounding
+    cfg = cfg_for(dim, n, mcs)
+    sym = okg.SchurContext(cfg)
+    full = okg.SchurContext(cfg, coarse_split=-1)
+    rng = np.random.default_rng(9)
+    for _ in range(3):
+        xc = rng.uniform(-1, 1, sym.level_sizes[-1])
+        a, b = sym.apply(_lib.OP_COARSE_SOLVE, xc), full.apply(_lib.OP_COARSE_SOLVE, xc)
+        assert relerr(a, b) <= 1e-14
+        assert np.array_equal(a, sym.apply(_lib.OP_COARSE_SOLVE, xc))  # deterministic
+    x = rng.uniform(-1, 1, sym.n)
+    assert relerr(sym.apply(_lib.OP_VCYCLE, x), full.apply(_lib.OP_VCYCLE, x)) <= 1e-13
+    sym.close()
+    full.close()
