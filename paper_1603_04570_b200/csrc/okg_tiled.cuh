@@ -272,8 +272,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       const int gi = cbi + ci, gj = cbj + cj, gk = cbk + ck;
       const bool in = gi <= a.gc.n && gk <= a.gc.n && (DIM == 2 || gj <= a.gc.n);
       const uint32_t lin = DIM == 3 ? (uint32_t)gi * a.gc.ps + (uint32_t)gj * a.gc.s + gk : (uint32_t)gi * a.gc.s + gk;
-      cp_async8(ct + e, a.x2 + lin, in);  // committed with the fine tile below
+      cp_async8(ct + e, a.x2 + lin, in);
     }
+    cp_commit();  // its own group: published by a barrier while the fine tile is in flight
   }
   // stage planes i0-1 .. i0+ni: every element by cp.async (LDGSTS, zero-fill outside
   // the box), all in flight at once together with the pointwise prefetch above --
@@ -320,9 +321,15 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     }
   }
   cp_commit();
+  if (CSTAGE) {
+    cp_wait<1>();     // this thread's coarse copies landed ...
+    __syncthreads();  // ... and everyone's: the coarse tile is visible
+  }
   cp_wait<0>();
   if (LOAD != L_PLAIN) {
-    __syncthreads();  // every copy (and the coarse tile) is visible
+    // the transform touches only this thread's own staged elements (the per-plane
+    // issue mapping), so no barrier is needed before it; L_PROLONG reads the coarse
+    // tile published above, the fallback path (no coarse tile) reads global memory
     // staging transform:  L_JAC0 r -> (w D^-1) r ;
     //                     L_PROLONG e -> e + P e_c  (x + t, multigrid.hpp:111-112)
     constexpr int CSI = CT::CJ * CT::CK, CSJ = CT::CK;
@@ -330,33 +337,57 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     const bool inner = i0 - 1 >= 1 && i0 + ni <= g.n - 1 && k0 - 1 >= 1 && k0 + TC::TK <= g.n - 1 &&
                        (DIM == 2 || (j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1));
     const double wd = a.omega * op.invd;
+    if (LOAD == L_JAC0 && inner) {
+      // branch-free: every slot of this thread (out-of-box / unused slots are never read)
 #pragma unroll
-    for (int p = 0; p < TI + 2; ++p) {
-      if (p >= ni + 2) continue;
-      const int ip = i0 - 1 + p;
+      for (int p = 0; p < TI + 2; ++p)
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (q + 1 < PER || tid + q * TC::NT < TC::PSZ) {
+            double& v = tile[p * TC::PSZ + tid + q * TC::NT];
+            v = wd * v;
+          }
+    } else if (CSTAGE) {
+      // coarse-tile offsets of this thread's slots, in-plane part (the plane part per p)
+      int cl[PER], cu[PER];
 #pragma unroll
       for (int q = 0; q < PER; ++q) {
-        if (!qin[q]) continue;
-        double& v = tile[p * TC::PSZ + tid + q * TC::NT];
-        if (LOAD == L_JAC0) {
-          if (inner) {
-            v = wd * v;
-          } else {
+        const int gj = qgj[q], gk = qgk[q];
+        cl[q] = (DIM == 3 ? ((gj >> 1) - cbj) * CSJ : 0) + ((gk >> 1) - cbk);
+        cu[q] = (DIM == 3 ? (((gj + 1) >> 1) - cbj) * CSJ : 0) + (((gk + 1) >> 1) - cbk);
+      }
+#pragma unroll
+      for (int p = 0; p < TI + 2; ++p) {
+        if (p >= ni + 2) break;  // CTA-uniform
+        const int ip = i0 - 1 + p;
+        const int pl = ((ip >> 1) - cbi) * CSI, pu = (((ip + 1) >> 1) - cbi) * CSI;
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          if (q + 1 < PER || tid + q * TC::NT < TC::PSZ) {
+            double& v = tile[p * TC::PSZ + tid + q * TC::NT];
+            const int lo = pl + cl[q], up = pu + cu[q];
+            const double t = lo == up ? ct[lo] : fma(0.5, ct[up], 0.5 * ct[lo]);
+            v = v + t;
+          }
+      }
+    } else {
+#pragma unroll
+      for (int p = 0; p < TI + 2; ++p) {
+        if (p >= ni + 2) continue;
+        const int ip = i0 - 1 + p;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          if (!qin[q]) continue;
+          double& v = tile[p * TC::PSZ + tid + q * TC::NT];
+          if (LOAD == L_JAC0) {
             const int cls = class_of<DIM>(g, ip, qgj[q], qgk[q]);
             const double invd = cls == Traits<DIM>::INTERIOR
                                     ? op.invd
                                     : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
             v = a.omega * invd * v;
+          } else {
+            v = v + prolong_at<DIM>(a.gc, a.x2, ip, qgj[q], qgk[q]);
           }
-        } else if (CSTAGE) {
-          const int gj = qgj[q], gk = qgk[q];
-          const int lo = ((ip >> 1) - cbi) * CSI + (DIM == 3 ? ((gj >> 1) - cbj) * CSJ : 0) + ((gk >> 1) - cbk);
-          const int up = (((ip + 1) >> 1) - cbi) * CSI + (DIM == 3 ? (((gj + 1) >> 1) - cbj) * CSJ : 0) +
-                         (((gk + 1) >> 1) - cbk);
-          const double t = lo == up ? ct[lo] : fma(0.5, ct[up], 0.5 * ct[lo]);
-          v = v + t;
-        } else {
-          v = v + prolong_at<DIM>(a.gc, a.x2, ip, qgj[q], qgk[q]);
         }
       }
     }

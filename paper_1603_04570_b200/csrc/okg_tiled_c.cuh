@@ -147,40 +147,25 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB_C) k_tile
       pb1[t] = (CNeeds<MODE>::B && ok) ? a.b[idx] : 0.0;
       pb2[t] = (MODE == TC_JAC_RES && ok) ? a.b[a.n2 + idx] : 0.0;
     }
+    // operand tiles by cp.async (zero-fill outside the box), all copies in flight at once
     const int per = (TI + 2) * TC::PSZ;
     const int tot1 = (ni + 2) * TC::PSZ;
-    const int total = NOPS * per;
-    constexpr int U = 8;
-    for (int base = tid; base < total; base += TC::NT * U) {
-      double vv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = base + u * TC::NT;
-        vv[u] = 0.0;
-        if (e < total) {
-          const int op = e >= per ? 1 : 0;
-          const int e2 = e - op * per;
-          if (e2 < tot1) {
-            const int p = e2 / TC::PSZ;
-            const int r = e2 - p * TC::PSZ;
-            const int hj = DIM == 3 ? r / TC::PW : 0;
-            const int hk = DIM == 3 ? r - hj * TC::PW : r;
-            const int gj = DIM == 3 ? j0 - 1 + hj : 0;
-            const int gk = k0 - 1 + hk;
-            const int ip = i0 - 1 + p;
-            if (gk <= g.n && gj <= g.n) {
-              const uint32_t lin = DIM == 3 ? (uint32_t)ip * g.ps + (uint32_t)gj * g.s + gk : (uint32_t)ip * g.s + gk;
-              vv[u] = __ldg((op ? a.v : a.x) + lin);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = base + u * TC::NT;
-        if (e < total) tile[e] = vv[u];
+    for (int op = 0; op < NOPS; ++op) {
+      const double* src = op ? a.v : a.x;
+      for (int e = tid; e < tot1; e += TC::NT) {
+        const int p = e / TC::PSZ;
+        const int r = e - p * TC::PSZ;
+        const int hj = DIM == 3 ? r / TC::PW : 0;
+        const int hk = DIM == 3 ? r - hj * TC::PW : r;
+        const int gj = DIM == 3 ? j0 - 1 + hj : 0;
+        const int gk = k0 - 1 + hk;
+        const uint32_t lin = (uint32_t)(i0 - 1 + p) * pstride + (DIM == 3 ? (uint32_t)gj * g.s : 0u) + gk;
+        cp_async8(tile + op * per + e, src + lin, gk <= g.n && gj <= g.n);
       }
     }
+    cp_commit();
+    cp_wait<0>();
     __syncthreads();
     if (active) {
 #pragma unroll
