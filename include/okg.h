@@ -87,6 +87,13 @@ typedef struct okg_params {
                                0 = default (each slab multiplies the rows of its own coarse
                                planes, then the planes are all-gathered), < 0 = every slab
                                multiplies all rows */
+  int32_t mg_collapse;      /* V(v,v) cycles only: the first coarse level with at most this many
+                               vertices, together with every level below it, is replaced at setup
+                               by the dense symmetric operator it applies (columns = the V-cycle
+                               of that level on unit vectors; packed lower block triangle), so
+                               the latency-bound bottom of each V-cycle is one HBM-streaming
+                               matvec; 0 = default (3D 1000, 2D 1100: the cluster tail's levels),
+                               < 0 = never */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -131,6 +138,7 @@ typedef struct okg_info {
   int32_t slab_ilo[16], slab_ihi[16]; /* owned x-planes [ilo, ihi) of the finest level per slab */
   int32_t tail_cluster;       /* CTAs in the tail's thread-block cluster */
   int32_t coarse_rows;        /* rows of the coarse inverse this slab multiplies */
+  int32_t collapse_level;     /* first level applied as one dense operator (-1: none) */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */

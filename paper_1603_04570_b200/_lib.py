@@ -48,6 +48,7 @@ class Params(C.Structure):
         ("tail_cluster", C.c_int32), ("cheb_fuse", C.c_int32),
         ("cheby_ssor", C.c_int32),
         ("coarse_split", C.c_int32),
+        ("mg_collapse", C.c_int32),
     ]
 
 
@@ -78,7 +79,7 @@ class Info(C.Structure):
         ("tail_start", C.c_int32), ("tiled_mask", C.c_int32),
         ("nslabs", C.c_int32), ("rep_level", C.c_int32),
         ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16), ("tail_cluster", C.c_int32),
-        ("coarse_rows", C.c_int32),
+        ("coarse_rows", C.c_int32), ("collapse_level", C.c_int32),
     ]
 
 

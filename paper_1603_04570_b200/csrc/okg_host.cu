@@ -134,6 +134,10 @@ struct okg_ctx {
   size_t coarse_ld = 0;
   int coarse_nb = 0;  // > 0: one slab, symmetric packed blocks (k_coarse_sym)
   double *coarse_R = nullptr, *coarse_C = nullptr;
+  // collapsed bottom of the V-cycle (okg_params.mg_collapse): level collapse_level and
+  // everything below it as one symmetric dense operator, packed like the coarse inverse
+  int collapse_level = -1, col_nb = 0;
+  double *col_A = nullptr, *col_R = nullptr, *col_C = nullptr;
   int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
   int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
   double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
@@ -674,7 +678,7 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
     launch(c, k_coarse_sym, (unsigned)(nb * (nb + 1) / 2), 256, 0, c->nc, (const double*)c->Ainv, b, c->coarse_R,
            c->coarse_C);
     note(c);
-    launch(c, k_coarse_sym_sum, (unsigned)nb, CB, 0, c->nc, nb, (const double*)c->coarse_R,
+    launch(c, k_coarse_sym_sum, (unsigned)nb, CB * CSEG, 0, c->nc, nb, (const double*)c->coarse_R,
            (const double*)c->coarse_C, y);
     note(c);
     return;
@@ -688,6 +692,46 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
     allgather_planes(c, last, L.ea);
     if (y != L.ea) copy(c, L.ea, y, (size_t)c->nc);
   }
+}
+
+template <int DIM>
+static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc);
+
+// see okg_params.mg_collapse: column i of the level-lc cycle operator is the cycle
+// applied to e_i; the (numerically symmetric) N x N result is packed as a lower block
+// triangle (k_coarse_pack takes its row-major upper triangle)
+template <int DIM>
+static void collapse_levels(okg_ctx* c, int lc) {
+  Level& L = c->lv[lc];
+  const int N = (int)L.g.N;
+  double* F = nullptr;
+  const size_t nn = (size_t)N * N;
+  cudaError_t e = cudaMalloc(&F, nn * sizeof(double));
+  if (e != cudaSuccess) THROW(OKG_ENOMEM, "cudaMalloc(%zu bytes) for the collapsed cycle: %s", nn * sizeof(double),
+                              cudaGetErrorString(e));
+  try {
+    for (int i = 0; i < N; ++i) {
+      k_unit<<<(N + 255) / 256, 256, 0, c->stream>>>(L.b, N, i);
+      CK(cudaGetLastError());
+      mg_level<DIM>(c, lc, L.b, L.x, false);
+      CK(cudaMemcpyAsync(F + (size_t)i * N, L.x, (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    const int nb = (N + CB - 1) / CB;
+    const size_t nblk = (size_t)nb * (nb + 1) / 2;
+    c->col_A = dalloc(c, nblk * CB * CB);
+    c->col_R = dalloc(c, nblk * CB);
+    c->col_C = dalloc(c, nblk * CB);
+    k_coarse_pack<<<148 * 8, 256, 0, c->stream>>>(N, nb, F, c->col_A);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    cudaFree(F);
+    throw;
+  }
+  cudaFree(F);
+  c->col_nb = (N + CB - 1) / CB;
+  c->collapse_level = lc;
+  c->tail_start = -1;  // the tail's levels are inside the collapsed operator
 }
 
 // Setup of the large coarsest level (nc > 2000): Cholesky + inverse of the dense
@@ -842,6 +886,16 @@ template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
   Level& L = c->lv[l];
   const int last = static_cast<int>(c->lv.size()) - 1;
+  if (l == c->collapse_level && !acc) {  // the whole cycle below l in one matvec
+    const int nb = c->col_nb;
+    launch(c, k_coarse_sym, (unsigned)(nb * (nb + 1) / 2), 256, 0, (int)L.g.N, (const double*)c->col_A, rhs, c->col_R,
+           c->col_C);
+    note(c);
+    launch(c, k_coarse_sym_sum, (unsigned)nb, CB * CSEG, 0, (int)L.g.N, nb, (const double*)c->col_R,
+           (const double*)c->col_C, out);
+    note(c);
+    return;
+  }
   if (l == c->tail_start && !acc && l > 0) {
     run_tail<DIM>(c, l, rhs, out);
     return;
@@ -2030,6 +2084,22 @@ static void build(okg_ctx* c) {
       }
     }
   }
+  // collapse the bottom of the V-cycle (okg_params.mg_collapse): the first coarse level
+  // with at most cmax vertices and every level below it apply a fixed linear map --
+  // symmetric for V(v,v) with damped Jacobi (the post-smoother is the pre-smoother's
+  // adjoint) -- so it is formed once (columns = that level's cycle on unit vectors,
+  // run through the existing kernels) and applied as one packed-symmetric matvec.
+  // Only on levels every slab holds whole (no communication below them).
+  if (p.mg_collapse >= 0 && p.mg_pre == p.mg_post && !c->coarse_big) {
+    const int64_t cmax = p.mg_collapse > 0 ? p.mg_collapse : (DIM == 3 ? 1000 : 1100);
+    int lc = -1;
+    for (size_t l = 1; l + 1 < c->lv.size(); ++l)
+      if ((int64_t)c->lv[l].g.N <= cmax) {
+        lc = (int)l;
+        break;
+      }
+    if (lc > 0 && (c->nslabs == 1 || lc >= c->L_rep)) collapse_levels<DIM>(c, lc);
+  }
   if (p.use_graphs) capture_graphs<DIM>(c);
   CK(cudaStreamSynchronize(c->stream));
 }
@@ -2628,6 +2698,7 @@ int okg_get_info(okg_ctx* h, okg_info* info) {
   info->tail_start = c->tail_start;
   info->tail_cluster = c->tail_start > 0 ? c->tail_cluster : 0;
   info->coarse_rows = c->coarse_big ? c->coarse_r1 - c->coarse_r0 : c->nc;
+  info->collapse_level = c->collapse_level;
   for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
     if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
   info->nslabs = h->handle ? h->nslabs : c->nslabs;

@@ -378,16 +378,45 @@ __global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __rest
   }
 }
 
-// y_r (r in block I) = sum_{J <= I} R(I,J)_r + sum_{K > I} C(K,I)_r
-__global__ void __launch_bounds__(CB) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
-                                                      const double* __restrict__ Cp, double* __restrict__ y) {
+// y_r (r in block I) = sum_{J <= I} R(I,J)_r + sum_{K > I} C(K,I)_r.  The nb terms
+// of a row are split into SEG contiguous segments (one warp-row of threads each,
+// loads issued 4 at a time), the segment sums then added in segment order: a fixed
+// order, so the result is deterministic.
+constexpr int CSEG = 4;
+__global__ void __launch_bounds__(CB * CSEG) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
+                                                              const double* __restrict__ Cp, double* __restrict__ y) {
   PDL_ENTRY();
-  const int I = blockIdx.x, t = threadIdx.x, r = I * CB + t;
-  double s = 0.0;
+  __shared__ double part[CSEG][CB];
+  const int I = blockIdx.x, t = threadIdx.x % CB, sg = threadIdx.x / CB;
   const size_t base = (size_t)I * (I + 1) / 2;
-  for (int J = 0; J <= I; ++J) s += R[(base + J) * CB + t];
-  for (int K = I + 1; K < nb; ++K) s += Cp[((size_t)K * (K + 1) / 2 + I) * CB + t];
-  if (r < nc) y[r] = s;
+  // term q (0..nb-1): q <= I -> R(I, q), else C(q, I)
+  auto term = [&](int q) -> double {
+    return q <= I ? __ldg(R + (base + q) * CB + t) : __ldg(Cp + ((size_t)q * (q + 1) / 2 + I) * CB + t);
+  };
+  const int per = (nb + CSEG - 1) / CSEG, q0 = sg * per, q1 = min(nb, q0 + per);
+  double s = 0.0;
+  int q = q0;
+  for (; q + 4 <= q1; q += 4) {
+    const double a0 = term(q), a1 = term(q + 1), a2 = term(q + 2), a3 = term(q + 3);
+    s += a0;
+    s += a1;
+    s += a2;
+    s += a3;
+  }
+  for (; q < q1; ++q) s += term(q);
+  part[sg][t] = s;
+  __syncthreads();
+  if (sg == 0) {
+    double r = part[0][t];
+#pragma unroll
+    for (int g = 1; g < CSEG; ++g) r += part[g][t];
+    if (I * CB + t < nc) y[I * CB + t] = r;
+  }
+}
+
+// setup: v = e_i (unit vector of length n)
+__global__ void k_unit(double* __restrict__ v, int n, int i) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) v[t] = t == i ? 1.0 : 0.0;
 }
 
 // setup: pack the lower block triangle of the full symmetric inverse (row-major upper
