@@ -362,7 +362,7 @@ def main():
     dom = kernels.get(DOMINANT)
     roofline = None
     if dom:
-        roofline = {"bound": "hbm", "kernel": f"{DOMINANT} (fine-level damped-Jacobi sweep on Shat_0, k_op<EPI_JACOBI>)",
+        roofline = {"bound": "hbm", "kernel": f"{DOMINANT} (fine-level damped-Jacobi sweep on Shat_0, k_tiled<{dim}, L_PLAIN, T_JACOBI, 8>)",
                     "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
                     "peak_source": peak_src, "traffic": None,
                     "alg_bytes_per_launch": dom["alg_bytes"], "avg_launch_us": dom["avg_us"]}

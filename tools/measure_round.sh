@@ -1,13 +1,20 @@
 #!/bin/bash
-# round-1 measurement refresh: bench lines, launch list, ncu of the dominant kernel
+# round measurement refresh: bench lines (3D 128^3, 400^3 slice of 800^3, 2D 2048^2,
+# reference arm), per-step launch lists, ncu --set full of the dominant kernel
 set -u
 mkdir -p gpurun_out
-cd paper_1603_04570_b200/csrc && make -s && cd ../..
-timeout 900 python bench.py > gpurun_out/r8_bench_3d128.json 2> gpurun_out/r8_bench_3d128.err
-timeout 900 python bench.py --workload c2_2d2048 --no-cpu-baseline > gpurun_out/r8_bench_2d2048.json 2> gpurun_out/r8_bench_2d2048.err
-timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r8_bench_ref.json 2> gpurun_out/r8_bench_ref.err
-bash tools/launch_list.sh r8_3d128 3 128 > /dev/null 2>&1
-KREGEX="k_tiled" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 128 5 0" bash tools/ncu_full.sh r8_smooth128 > /dev/null 2>&1
-ncu -i gpurun_out/r8_smooth128.ncu-rep --page raw --csv > gpurun_out/r8_smooth128_raw.csv 2>/dev/null
-tail -c 600 gpurun_out/r8_bench_3d128.json; echo; tail -c 300 gpurun_out/r8_bench_2d2048.json; echo; tail -c 300 gpurun_out/r8_bench_ref.json; echo
-head -5 gpurun_out/ll_r8_3d128.summary.txt
+P=${PFX:-m}
+timeout 900 python bench.py > gpurun_out/${P}_bench_3d128.json 2> gpurun_out/${P}_bench_3d128.err
+timeout 900 python bench.py --workload c5_3d800 --steps 3 > gpurun_out/${P}_bench_3d400.json 2> gpurun_out/${P}_bench_3d400.err
+timeout 900 python bench.py --workload c2_2d2048 --no-cpu-baseline > gpurun_out/${P}_bench_2d2048.json 2> gpurun_out/${P}_bench_2d2048.err
+timeout 900 python bench.py --impl reference > gpurun_out/${P}_bench_ref.json 2> gpurun_out/${P}_bench_ref.err
+bash tools/launch_list.sh ${P}_3d128 3 128 > /dev/null 2>&1
+OKG_MIN_COARSE=17576 bash tools/launch_list.sh ${P}_3d400 3 400 > /dev/null 2>&1
+KREGEX="k_tiled" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 128 5 0" bash tools/ncu_full.sh ${P}_smooth128 > /dev/null 2>&1
+OKG_MIN_COARSE=17576 KREGEX="k_tiled" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 400 5 0" bash tools/ncu_full.sh ${P}_smooth400 > /dev/null 2>&1
+for f in ${P}_smooth128 ${P}_smooth400; do
+  ncu -i gpurun_out/$f.ncu-rep --page raw --csv > gpurun_out/${f}_raw.csv 2>/dev/null
+  ncu -i gpurun_out/$f.ncu-rep --page details --csv > gpurun_out/${f}_details.csv 2>/dev/null
+done
+for f in gpurun_out/${P}_bench_*.json; do echo $f; tail -c 400 $f; echo; done
+head -12 gpurun_out/ll_${P}_3d128.summary.txt gpurun_out/ll_${P}_3d400.summary.txt
