@@ -699,8 +699,11 @@ __device__ __forceinline__ double ring_row(const Op<DIM>& op, int cls, const dou
   return s;
 }
 
-// Each state ring (u+, w+, u, w) is loaded once; every M/K row and N(u+)
-// is evaluated from registers.
+// The u+ ring is held in registers (N(u+) needs all of it); the u, w+, w rings
+// are streamed slot by slot into their M/K row sums -- each sum still runs over
+// the slots in ascending order with the same operands (bit-identical to forming
+// every ring first), at a third of the registers (164 -> ~64: 4x the resident
+// warps for this gather-bound kernel).
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_residual(Grid g, Op<DIM> Mop, Op<DIM> Kop, Nonlin nl, ResArgs a,
                                                  Reduce red) {
@@ -710,21 +713,35 @@ __global__ void __launch_bounds__(BS) k_residual(Grid g, Op<DIM> Mop, Op<DIM> Ko
   double v[2] = {0.0, 0.0};
   if (idx < g.hi) {
     const Node<DIM> nd = locate<DIM>(g, idx);
-    const double bi = nd.cls == Traits<DIM>::INTERIOR ? a.b_int : __ldg(a.b_tab + nd.cls);
-    double un[NO], wn[NO], uo[NO], wo[NO], du[NO];
+    const bool inter = nd.cls == Traits<DIM>::INTERIOR;
+    const double bi = inter ? a.b_int : __ldg(a.b_tab + nd.cls);
+    const double* tm = Mop.tab + nd.cls * (NO + 1);
+    const double* tk = Kop.tab + nd.cls * (NO + 1);
+    double un[NO];
     load_ring<DIM>(g, idx, nd.cls, a.un, un);
-    load_ring<DIM>(g, idx, nd.cls, a.wn, wn);
-    load_ring<DIM>(g, idx, nd.cls, a.uo, uo);
-    load_ring<DIM>(g, idx, nd.cls, a.wo, wo);
+    double mdu = 0.0, muo = 0.0, kwn = 0.0, mwn = 0.0, kwo = 0.0, mun = 0.0, kun = 0.0;
 #pragma unroll
-    for (int o = 0; o < NO; ++o) du[o] = un[o] - uo[o];
-    const double mdu = ring_row<DIM>(Mop, nd.cls, du);
-    const double kwn = ring_row<DIM>(Kop, nd.cls, wn);
-    const double mun = ring_row<DIM>(Mop, nd.cls, un);
-    const double kwo = ring_row<DIM>(Kop, nd.cls, wo);
-    const double muo = ring_row<DIM>(Mop, nd.cls, uo);
-    const double mwn = ring_row<DIM>(Mop, nd.cls, wn);
-    const double kun = ring_row<DIM>(Kop, nd.cls, un);
+    for (int o = 0; o < NO; ++o) {
+      const bool ok = inter || slot_ok<DIM>(nd.cls, o);
+      const int j = (int)idx + (ok ? g.off[o] : 0);
+      const double uo = ok ? __ldg(a.uo + j) : 0.0;
+      const double wn = ok ? __ldg(a.wn + j) : 0.0;
+      const double wo = ok ? __ldg(a.wo + j) : 0.0;
+      const double wm = inter ? Mop.w[o] : __ldg(tm + o);
+      const double wk = inter ? Kop.w[o] : __ldg(tk + o);
+      const double du = un[o] - uo;
+      if (inter || wm != 0.0) {
+        mdu = fma(wm, du, mdu);
+        mun = fma(wm, un[o], mun);
+        muo = fma(wm, uo, muo);
+        mwn = fma(wm, wn, mwn);
+      }
+      if (inter || wk != 0.0) {
+        kwn = fma(wk, wn, kwn);
+        kwo = fma(wk, wo, kwo);
+        kun = fma(wk, un[o], kun);
+      }
+    }
     const double nlu = nonlinear_row<DIM>(g, nd, un, nl);
     const double fn = kwn + a.sigma * (mun + (-a.m) * bi);
     const double fo = kwo + a.sigma * (muo + (-a.m) * bi);

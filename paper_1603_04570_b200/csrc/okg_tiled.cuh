@@ -372,15 +372,21 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       }
     } else {
 #pragma unroll
+      // class digits of this thread's slots (j, k part once; the plane part per p)
+      int qcjk[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) qcjk[q] = DIM == 3 ? cdig(qgj[q], g.n) * 3 + cdig(qgk[q], g.n) : cdig(qgk[q], g.n);
+#pragma unroll
       for (int p = 0; p < TI + 2; ++p) {
         if (p >= ni + 2) continue;
         const int ip = i0 - 1 + p;
+        const int cip = cdig(ip, g.n) * (DIM == 3 ? 9 : 3);
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
           if (!qin[q]) continue;
           double& v = tile[p * TC::PSZ + tid + q * TC::NT];
           if (LOAD == L_JAC0) {
-            const int cls = class_of<DIM>(g, ip, qgj[q], qgk[q]);
+            const int cls = cip + qcjk[q];
             const double invd = cls == Traits<DIM>::INTERIOR
                                     ? op.invd
                                     : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
