@@ -371,7 +371,6 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
           }
       }
     } else {
-#pragma unroll
       // class digits of this thread's slots (j, k part once; the plane part per p)
       int qcjk[PER];
 #pragma unroll
