@@ -94,6 +94,11 @@ typedef struct okg_params {
                                the latency-bound bottom of each V-cycle is one HBM-streaming
                                matvec; 0 = default (3D 1000, 2D 1100: the cluster tail's levels),
                                < 0 = never */
+  int32_t mg_cluster;       /* V(2,2), one slab, collapsed bottom: from the first level with at most
+                               this many vertices down to the collapsed bottom, the V-cycle runs as
+                               ONE 16-CTA thread-block-cluster kernel with the levels in distributed
+                               shared memory (okg_cluster.cuh); bit-identical, but measured slower
+                               than the chained level kernels, so opt-in: <= 0 = never (default) */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -139,6 +144,7 @@ typedef struct okg_info {
   int32_t tail_cluster;       /* CTAs in the tail's thread-block cluster */
   int32_t coarse_rows;        /* rows of the coarse inverse this slab multiplies */
   int32_t collapse_level;     /* first level applied as one dense operator (-1: none) */
+  int32_t mc_start;           /* first level of the cluster V-cycle (-1: none) */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */
@@ -149,7 +155,7 @@ enum okg_op {
   OKG_OP_SHAT = 3,           /* level operator Shat_l            multigrid.hpp:55-66   */
   OKG_OP_PROLONG = 4,        /* P_l : level l+1 -> level l       mesh.hpp:169          */
   OKG_OP_RESTRICT = 5,       /* P_l^T : level l -> level l+1     sparse.hpp:159        */
-  OKG_OP_VCYCLE = 6,         /* v_cycle                          multigrid.hpp:124     */
+  OKG_OP_VCYCLE = 6,         /* v_cycle (mg_cycle on `level`)    multigrid.hpp:97-129  */
   OKG_OP_SHAT_INV = 7,       /* apply_shat_inv                   multigrid.hpp:133     */
   OKG_OP_CHEB_M = 8,         /* apply_M_inv                      precond.hpp:185       */
   OKG_OP_CHEB_A = 9,         /* apply_A_inv                      precond.hpp:191       */

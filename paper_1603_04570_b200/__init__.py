@@ -78,7 +78,7 @@ class SolverConfig:
                   tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
                   mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
                   tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0,
-                  mg_collapse: int = 0) -> _lib.Params:
+                  mg_collapse: int = 0, mg_cluster: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -98,6 +98,7 @@ class SolverConfig:
         p.cheb_fuse = cheb_fuse
         p.coarse_split = coarse_split
         p.mg_collapse = mg_collapse
+        p.mg_cluster = mg_cluster
         p.cheby_ssor = 1 if self.cheby_precond == "ssor" else 0
         return p
 
@@ -306,7 +307,8 @@ class SchurContext:
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
                  pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
                  rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None,
-                 tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0, mg_collapse: int = 0):
+                 tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0, mg_collapse: int = 0,
+                 mg_cluster: int = 0):
         """nslabs > 1: x-plane slab decomposition, one host thread + stream per
         slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
         `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
@@ -317,7 +319,7 @@ class SchurContext:
         self.handle = C.c_void_p()
         params = cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl, mg_fuse,
                                nslabs, slab_devices, tail_cluster, cheb_fuse, coarse_split,
-                               mg_collapse)
+                               mg_collapse, mg_cluster)
         if rank is None:
             check(lib.okg_create(C.byref(params), C.byref(self.handle)))
         else:
@@ -346,6 +348,7 @@ class SchurContext:
         self.tiled_levels = [l for l in range(self.levels) if (info.tiled_mask >> l) & 1]
         self.coarse_rows = int(info.coarse_rows)
         self.collapse_level = int(info.collapse_level)
+        self.mc_start = int(info.mc_start)
         self.nslabs = int(info.nslabs)
         self.rep_level = int(info.rep_level)
         self.slab_planes = [(int(info.slab_ilo[r]), int(info.slab_ihi[r])) for r in range(self.nslabs)]
@@ -367,7 +370,7 @@ class SchurContext:
 
     # ---- per-operator entry points (host arrays in/out) ----
     def _out_size(self, kind: int, level: int) -> int:
-        if kind == _lib.OP_SHAT or kind == _lib.OP_PROLONG:
+        if kind in (_lib.OP_SHAT, _lib.OP_PROLONG, _lib.OP_VCYCLE):
             return self.level_sizes[level]
         if kind == _lib.OP_RESTRICT:
             return self.level_sizes[level + 1]

@@ -49,6 +49,7 @@ class Params(C.Structure):
         ("cheby_ssor", C.c_int32),
         ("coarse_split", C.c_int32),
         ("mg_collapse", C.c_int32),
+        ("mg_cluster", C.c_int32),
     ]
 
 
@@ -80,6 +81,7 @@ class Info(C.Structure):
         ("nslabs", C.c_int32), ("rep_level", C.c_int32),
         ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16), ("tail_cluster", C.c_int32),
         ("coarse_rows", C.c_int32), ("collapse_level", C.c_int32),
+        ("mc_start", C.c_int32),
     ]
 
 

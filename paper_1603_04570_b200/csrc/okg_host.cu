@@ -141,6 +141,10 @@ struct okg_ctx {
   int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
   int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
   double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
+  // cluster V-cycle (okg_cluster.cuh): levels mc_start .. collapse_level-1 and the
+  // collapsed bottom in one 16-CTA cluster launch (-1: none)
+  int mc_start = -1;
+  double* mc_tab = nullptr;
   double b_int = 0;
   double* b_tab = nullptr;
   Nonlin nl;
@@ -618,7 +622,10 @@ static void make_tiling(okg_ctx* c, Level& L) {
     tt.ichunk = ichunk;
     tt.ncore = base * ((nci + ichunk - 1) / ichunk);
   };
-  chunking(8, t);
+#ifndef OKG_FINE_TI
+#define OKG_FINE_TI 8
+#endif
+  chunking(OKG_FINE_TI, t);
   std::vector<uint32_t> bnd;
   const int s = n + 1;
   if (DIM == 3) {
@@ -855,6 +862,42 @@ static void run_tail(okg_ctx* c, int l0, const double* rhs, double* out) {
   note(c);
 }
 
+// levels mc_start .. collapse_level-1 + the collapsed bottom in one cluster launch
+// (okg_cluster.cuh); instantiated for power-of-two levels ending at the default
+// collapse level (3D 9^3, 2D 33^2)
+template <int DIM, class F>
+static bool mc_dispatch(int n0, int nl, F&& f) {
+  using I = std::integral_constant<int, 1>;
+  using II = std::integral_constant<int, 2>;
+  if constexpr (DIM == 3) {
+    if (n0 == 32 && nl == 2) f(std::integral_constant<int, 32>{}, II{});
+    else if (n0 == 16 && nl == 1) f(std::integral_constant<int, 16>{}, I{});
+    else return false;
+  } else {
+    if (n0 == 256 && nl == 3) f(std::integral_constant<int, 256>{}, std::integral_constant<int, 3>{});
+    else if (n0 == 128 && nl == 2) f(std::integral_constant<int, 128>{}, II{});
+    else if (n0 == 64 && nl == 1) f(std::integral_constant<int, 64>{}, I{});
+    else return false;
+  }
+  return true;
+}
+
+template <int DIM>
+static void run_mc(okg_ctx* c, int l0, const double* rhs, double* out) {
+  MCArgs<DIM> A;
+  std::memset(&A, 0, sizeof A);
+  A.tabs = c->mc_tab;
+  A.omega = c->p.mg_omega;
+  A.rhs = rhs;
+  A.out = out;
+  A.colA = c->col_A;
+  mc_dispatch<DIM>(c->lv[l0].g.n, c->collapse_level - l0, [&](auto N0, auto NL) {
+    constexpr int n0 = decltype(N0)::value, nl = decltype(NL)::value;
+    launch_cluster(c, k_mg_cluster<DIM, n0, nl>, (unsigned)MC_C, MC_NT, mc_smem_bytes<DIM, n0, nl>(), A);
+  });
+  note(c);
+}
+
 template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc);
 
@@ -886,6 +929,10 @@ template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
   Level& L = c->lv[l];
   const int last = static_cast<int>(c->lv.size()) - 1;
+  if (l == c->mc_start && !acc) {
+    run_mc<DIM>(c, l, rhs, out);
+    return;
+  }
   if (l == c->collapse_level && !acc) {  // the whole cycle below l in one matvec
     const int nb = c->col_nb;
     launch(c, k_coarse_sym, (unsigned)(nb * (nb + 1) / 2), 256, 0, (int)L.g.N, (const double*)c->col_A, rhs, c->col_R,
@@ -2100,6 +2147,63 @@ static void build(okg_ctx* c) {
       }
     if (lc > 0 && (c->nslabs == 1 || lc >= c->L_rep)) collapse_levels<DIM>(c, lc);
   }
+  // cluster V-cycle above the collapsed bottom (okg_params.mg_cluster, okg_cluster.cuh)
+  // (opt-in: measured slower than the PDL-chained level kernels)
+  if (p.mg_cluster > 0 && c->collapse_level > 1 && c->nslabs == 1 && p.mg_pre == 2 && p.mg_post == 2) {
+    const int64_t vmax = p.mg_cluster;
+    for (int l = 1; l < c->collapse_level; ++l) {
+      if ((int64_t)c->lv[l].g.N > vmax) continue;
+      bool ok = false;
+      mc_dispatch<DIM>(c->lv[l].g.n, c->collapse_level - l, [&](auto N0, auto NL) {
+        constexpr int n0 = decltype(N0)::value, nl = decltype(NL)::value;
+        auto k = k_mg_cluster<DIM, n0, nl>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mc_smem_bytes<DIM, n0, nl>()) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+          cudaGetLastError();
+          return;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(MC_C);
+        cfg.blockDim = dim3(MC_NT);
+        cfg.dynamicSmemBytes = mc_smem_bytes<DIM, n0, nl>();
+        cudaLaunchAttribute at;
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = MC_C;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k, &cfg) != cudaSuccess) cudaGetLastError();
+        ok = ncl > 0;
+      });
+      if (!ok) break;
+      // tables: the cluster levels' class rows, then the restriction weights (as the tail)
+      const int NO = Traits<DIM>::NOFF, NCL = Traits<DIM>::NCLS;
+      const int nl = c->collapse_level - l;
+      std::vector<double> tt((size_t)mc_table_doubles<DIM>(nl), 0.0);
+      for (int q = 0; q < nl; ++q) {
+        const std::vector<double>& h = c->lv[l + q].shat.htab;
+        std::copy(h.begin(), h.end(), tt.begin() + (size_t)q * NCL * (NO + 1));
+      }
+      for (int cl = 0; cl < NCL; ++cl)
+        for (int o = 0; o < NO; ++o) {
+          bool in = true;
+          int cc = cl;
+          for (int d = DIM - 1; d >= 0; --d) {
+            const int cd = cc % 3, od = off_comp(DIM, o, d);
+            cc /= 3;
+            in = in && !(cd == 0 && od < 0) && !(cd == 2 && od > 0);
+          }
+          tt[(size_t)nl * NCL * (NO + 1) + cl * NO + o] = in ? (o == NO / 2 ? 1.0 : 0.5) : 0.0;
+        }
+      c->mc_tab = dalloc(c, tt.size());
+      CK(cudaMemcpyAsync(c->mc_tab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      c->mc_start = l;
+      break;
+    }
+  }
   if (p.use_graphs) capture_graphs<DIM>(c);
   CK(cudaStreamSynchronize(c->stream));
 }
@@ -2206,7 +2310,10 @@ static void apply_impl(okg_ctx* c, int kind, int level, const double* x, double*
       launch(c, k_restrict<DIM>, nblk(c->lv[level + 1].g.N), BS, 0, c->lv[level].g, c->lv[level + 1].g, x, y);
       note(c);
       break;
-    case OKG_OP_VCYCLE: mg_level<DIM>(c, 0, x, y, false); break;
+    case OKG_OP_VCYCLE:  // mg_cycle on level `level` (v_cycle: level 0, multigrid.hpp:124-129)
+      if (level < 0 || level >= nlev || (level > 0 && c->nslabs > 1)) THROW(OKG_EINVAL, "level out of range");
+      mg_level<DIM>(c, level, x, y, false);
+      break;
     case OKG_OP_SHAT_INV: shat_inv<DIM>(c, x, y, c->p.mg_cycles); break;
     case OKG_OP_CHEB_M: cheb<DIM>(c, c->M, x, y); break;
     case OKG_OP_CHEB_A: cheb<DIM>(c, c->A, x, y); break;
@@ -2508,7 +2615,7 @@ static void apply_sizes(okg_ctx* c, int kind, int level, size_t& nin, size_t& no
   nin = nout = c->N;
   switch (kind) {
     case OKG_OP_BLOCK: case OKG_OP_JACOBIAN: nin = nout = 2 * (size_t)c->N; break;
-    case OKG_OP_SHAT:
+    case OKG_OP_SHAT: case OKG_OP_VCYCLE:
       if (level < 0 || level >= nlev) THROW(OKG_EINVAL, "level out of range");
       nin = nout = c->lv[level].g.N;
       break;
@@ -2699,6 +2806,7 @@ int okg_get_info(okg_ctx* h, okg_info* info) {
   info->tail_cluster = c->tail_start > 0 ? c->tail_cluster : 0;
   info->coarse_rows = c->coarse_big ? c->coarse_r1 - c->coarse_r0 : c->nc;
   info->collapse_level = c->collapse_level;
+  info->mc_start = c->mc_start;
   for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
     if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
   info->nslabs = h->handle ? h->nslabs : c->nslabs;
@@ -2948,7 +3056,7 @@ int okg_apply_host(okg_ctx* c, int32_t kind, int32_t level, const double* x, dou
   if (!c || !x || !y) return fail(OKG_EINVAL, "okg_apply_host: null argument");
   if (kind < OKG_OP_M || kind > OKG_OP_SSOR_M) return fail(OKG_EINVAL, "okg_apply_host: unknown kind %d", kind);
   const bool level0 = !(kind == OKG_OP_PROLONG || kind == OKG_OP_RESTRICT || kind == OKG_OP_COARSE_SOLVE ||
-                        (kind == OKG_OP_SHAT && level != 0));
+                        ((kind == OKG_OP_SHAT || kind == OKG_OP_VCYCLE) && level != 0));
   if (c->handle && !level0)
     return fail(OKG_EINVAL, "okg_apply_host: kind %d on level %d needs a one-slab context", kind, level);
   return each_slab(c, [&](okg_ctx* s) {

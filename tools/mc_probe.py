@@ -1,0 +1,25 @@
+"""V-cycle of one coarse level repeated (for ncu): python tools/mc_probe.py DIM N CLUSTER [reps]
+prints the level the cycle runs on; OKG_* knobs as tools/profile_step.py."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1603_04570_b200 as okg  # noqa: E402
+from paper_1603_04570_b200 import _lib  # noqa: E402
+
+dim, n, knob = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
+cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30)
+ref = okg.SchurContext(cfg, mg_cluster=int(os.environ.get("OKG_PROBE_LEVEL_KNOB", "0")))
+lvl = ref.mc_start
+ref.close()
+ctx = okg.SchurContext(cfg, mg_cluster=knob)
+print(f"level={lvl} n={ctx.level_n[lvl]} mc_start={ctx.mc_start}", flush=True)
+x = okg.DeviceArray.from_numpy(np.random.default_rng(0).uniform(-1, 1, ctx.level_sizes[lvl]))
+y = okg.DeviceArray(ctx.level_sizes[lvl])
+for _ in range(reps):
+    ctx.apply_dev(_lib.OP_VCYCLE, x, y, lvl)
+_lib.check(_lib.lib.okg_device_synchronize())
+print("ok", float(np.abs(y.numpy()).sum()))
