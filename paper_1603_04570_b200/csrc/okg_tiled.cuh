@@ -308,16 +308,33 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       }
     }
   } else {
+    // linear tile order, e = tid + m NT: the tile coordinates (p, hj, hk) and the global
+    // offset advance incrementally (NT = DJ PW + DK; at most one carry per coordinate),
+    // no per-element division
     const int total = (ni + 2) * TC::PSZ;
+    constexpr int PH = TC::PSZ / TC::PW;  // rows per staged plane (1 in 2D)
+    constexpr int DJ = TC::NT / TC::PW, DK = TC::NT % TC::PW;
+    static_assert(DJ + 1 <= PH || PH == 1, "one carry per step");
+    const int rs = DIM == 3 ? g.s : 0;  // global stride of a tile row
+    int hk = tid % TC::PW, hj = tid / TC::PW;  // tid < PSZ: plane 0
+    const int kmax = g.n - (k0 - 1), jmax = DIM == 3 ? g.n - (j0 - 1) : 0;
+    uint32_t lin = (uint32_t)(i0 - 1) * pstride + (DIM == 3 ? (uint32_t)(j0 - 1 + hj) * g.s : 0u) + (k0 - 1 + hk);
+    const int dlin = DJ * rs + DK, cjk = rs - TC::PW, cpj = (int)pstride - PH * rs;
     for (int e = tid; e < total; e += TC::NT) {
-      const int p = e / TC::PSZ;
-      const int r = e - p * TC::PSZ;
-      const int hj = DIM == 3 ? r / TC::PW : 0;
-      const int hk = DIM == 3 ? r - hj * TC::PW : r;
-      const int gj = DIM == 3 ? j0 - 1 + hj : 0;
-      const int gk = k0 - 1 + hk;
-      const uint32_t lin = (uint32_t)(i0 - 1 + p) * pstride + (DIM == 3 ? (uint32_t)gj * g.s : 0u) + gk;
-      cp_async8(tile + e, a.x + lin, gk <= g.n && gj <= g.n);
+      cp_async8(tile + e, a.x + lin, hk <= kmax && hj <= jmax);
+      hk += DK;
+      hj += DJ;
+      int d = dlin;
+      if (hk >= TC::PW) {
+        hk -= TC::PW;
+        ++hj;
+        d += cjk;
+      }
+      if (hj >= PH) {
+        hj -= PH;
+        d += cpj;
+      }
+      lin += (uint32_t)d;
     }
   }
   cp_commit();
