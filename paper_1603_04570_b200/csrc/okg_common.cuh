@@ -20,18 +20,33 @@
 namespace okg {
 
 // Programmatic dependent launch (Hopper/Blackwell): every kernel is launched
-// with cudaLaunchAttributeProgrammaticStreamSerialization, waits for its
-// predecessor grid's completion (and memory) before touching global memory,
-// and immediately lets its own dependent grid be scheduled, so launch latency
-// and CTA ramp-up overlap the predecessor's tail.  griddepcontrol.wait is a
-// no-op for a kernel launched without the attribute.
+// with cudaLaunchAttributeProgrammaticStreamSerialization and waits for its
+// predecessor grid's completion (and memory) in griddepcontrol.wait before
+// touching global memory, so launch latency and CTA ramp-up overlap the
+// predecessor's tail.  Where a CTA lets its dependent grid be scheduled
+// (griddepcontrol.launch_dependents) is OKG_PDL_TRIGGER:
+//   2 (default): the multi-wave fine-level kernels (k_tiled, k_tiled_c) trigger
+//      once their operand tile is staged, every other kernel at exit;
+//   1: every kernel right at entry;   0: every kernel at exit.
+// Measured (per-step, graphs on, one B200): 3D 128^3 50.9 (1) / 49.7 (0) /
+// 49.2 ms (2); 2D 2048^2 62.8 / 62.8 / 62.7 ms; 400^3 within 0.5 %.  An early
+// trigger lets the dependent grid's CTAs take SM slots (spinning in
+// griddepcontrol.wait) that the primary's later waves need.
+// griddepcontrol.wait is a no-op for a kernel launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#ifndef OKG_PDL_TRIGGER
+#define OKG_PDL_TRIGGER 2
+#endif
+#if OKG_PDL_TRIGGER == 1
 #define PDL_ENTRY() \
   do {              \
     pdl_wait();     \
     pdl_trigger();  \
   } while (0)
+#else
+#define PDL_ENTRY() pdl_wait()
+#endif
 
 template <int DIM>
 struct Traits;

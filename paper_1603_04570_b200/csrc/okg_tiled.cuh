@@ -415,6 +415,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     }
   }
   __syncthreads();
+#if OKG_PDL_TRIGGER == 2
+  pdl_trigger();  // operands staged: the dependent grid may start its prologue
+#endif
   if (!active) return;
   // all TI vertex chains are computed unconditionally (no branch between them, so
   // their dependent FMA chains interleave); only the stores are predicated

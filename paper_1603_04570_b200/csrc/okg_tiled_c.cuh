@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB_C) k_tile
     cp_commit();
     cp_wait<0>();
     __syncthreads();
+#if OKG_PDL_TRIGGER == 2
+    pdl_trigger();  // operands staged: the dependent grid may start its prologue
+#endif
     if (active) {
 #pragma unroll
       for (int t = 0; t < TI; ++t) {

@@ -18,6 +18,7 @@ cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_rest
 ctx = okg.SchurContext(cfg, tiled_min_n=int(os.environ.get("OKG_TILED", "0")),
                        tail_max_vertices=int(os.environ.get("OKG_TAIL", "0")),
                        pdl=os.environ.get("OKG_PDL", "1") == "1",
+                       use_graphs=os.environ.get("OKG_GRAPHS", "1") == "1",
                        mg_fuse=int(os.environ.get("OKG_FUSE", "0")),
                        tail_cluster=int(os.environ.get("OKG_TAILC", "0")),
                        cheb_fuse=int(os.environ.get("OKG_CHEB2", "0")),
