@@ -27,11 +27,13 @@ namespace okg {
 // (griddepcontrol.launch_dependents) is OKG_PDL_TRIGGER:
 //   2 (default): the multi-wave fine-level kernels (k_tiled, k_tiled_c) trigger
 //      once their operand tile is staged, every other kernel at exit;
-//   1: every kernel right at entry;   0: every kernel at exit.
-// Measured (per-step, graphs on, one B200): 3D 128^3 50.9 (1) / 49.7 (0) /
-// 49.2 ms (2); 2D 2048^2 62.8 / 62.8 / 62.7 ms; 400^3 within 0.5 %.  An early
-// trigger lets the dependent grid's CTAs take SM slots (spinning in
-// griddepcontrol.wait) that the primary's later waves need.
+//   1: the other kernels right at entry (k_tiled / k_tiled_c at exit);
+//   0: every kernel at exit.
+// Measured (per-step, graphs on, one B200; "all at entry" was the old default):
+// 3D 128^3 all-at-entry 50.9 / 0: 49.7 / 1: 50.9 / 2: 49.2 ms; 2D 2048^2
+// 62.8 / 62.8 / 62.7 / 62.7 ms; 400^3 within 0.5 %.  An early trigger lets the
+// dependent grid's CTAs take SM slots (spinning in griddepcontrol.wait) that
+// the primary's later waves need.
 // griddepcontrol.wait is a no-op for a kernel launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

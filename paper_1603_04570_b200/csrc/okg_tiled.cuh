@@ -223,7 +223,7 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
 // thread computes TI vertices along x.  Extra CTAs take the boundary list.
 template <int DIM, int LOAD, int EPI, int TI>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
-  PDL_ENTRY();
+  pdl_wait();  // (the dependent grid is released below, once the tile is staged)
   using TC = TileCfg<DIM>;
   constexpr int NO = Traits<DIM>::NOFF;
   const int tid = threadIdx.x;

@@ -99,7 +99,7 @@ __device__ __forceinline__ void c_vertex(const Grid& g, const Op<DIM>& Mop, cons
 template <int DIM, int MODE, int TI>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB_C) k_tiled_c(Grid g, Op<DIM> Mop, Op<DIM> Kop, Op<DIM> Aop,
                                                               Tiling tl, CTArgs a, Reduce red) {
-  PDL_ENTRY();
+  pdl_wait();  // (the dependent grid is released below, once the tile is staged)
   using TC = TileCfg<DIM>;
   constexpr int NO = Traits<DIM>::NOFF;
   constexpr int NOPS = CNeeds<MODE>::NOPS;
