@@ -79,8 +79,9 @@ typedef struct okg_params {
                                device `device + r` (peer copies over NVLink) */
   int32_t tail_cluster;     /* CTAs in the tail's cluster (they split the rows of the dense
                                coarse inverse): 0 = default (enough for <= 96 KB each), 1..16 */
-  int32_t cheb_fuse;        /* Chebyshev steps two per pass (2D, one slab): 0 = default (on),
-                               < 0 = one step per pass */
+  int32_t cheb_fuse;        /* Chebyshev steps two per pass (2D, one slab; bit-identical):
+                               > 0 = on with this many rows per tile (4 measured best),
+                               <= 0 = one step per pass (default) */
   int32_t cheby_ssor;       /* SolverConfig::cheby_precond: 0 = "jacobi", 1 = "ssor" (SSOR
                                sweeps as hyperplane wavefronts, one slab only) */
   int32_t coarse_split;     /* coarsest level above 2000 unknowns (device-factorised inverse):

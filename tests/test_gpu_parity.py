@@ -368,7 +368,7 @@ def test_two_step_chebyshev_bit_identical(n, k):
     rng = np.random.default_rng(n + k)
     x = rng.uniform(-1, 1, (n + 1) ** 2)
     outs = []
-    for fuse in (-1, 0):
+    for fuse in (-1, 4):
         ctx = okg.SchurContext(cfg, cheb_fuse=fuse)
         ctx.linearize(okg.seeded_ic(ctx.n, 1, 0.0))
         outs.append([ctx.apply(kind, x) for kind in (_lib.OP_CHEB_M, _lib.OP_CHEB_A, _lib.OP_SCHUR)])
