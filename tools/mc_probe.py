@@ -1,5 +1,6 @@
 """V-cycle of one coarse level repeated (for ncu): python tools/mc_probe.py DIM N CLUSTER [reps]
-prints the level the cycle runs on; OKG_* knobs as tools/profile_step.py."""
+CLUSTER = okg_params.mg_cluster of the measured context; the level is OKG_PROBE_LEVEL, or
+the one a cluster knob OKG_PROBE_LEVEL_KNOB (default 40000) would start on."""
 import os
 import sys
 
@@ -12,9 +13,12 @@ from paper_1603_04570_b200 import _lib  # noqa: E402
 dim, n, knob = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
 cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30)
-ref = okg.SchurContext(cfg, mg_cluster=int(os.environ.get("OKG_PROBE_LEVEL_KNOB", "0")))
-lvl = ref.mc_start
-ref.close()
+if "OKG_PROBE_LEVEL" in os.environ:  # explicit level
+    lvl = int(os.environ["OKG_PROBE_LEVEL"])
+else:  # the level a cluster knob would start on
+    ref = okg.SchurContext(cfg, mg_cluster=int(os.environ.get("OKG_PROBE_LEVEL_KNOB", "40000")))
+    lvl = ref.mc_start
+    ref.close()
 ctx = okg.SchurContext(cfg, mg_cluster=knob)
 print(f"level={lvl} n={ctx.level_n[lvl]} mc_start={ctx.mc_start}", flush=True)
 x = okg.DeviceArray.from_numpy(np.random.default_rng(0).uniform(-1, 1, ctx.level_sizes[lvl]))
