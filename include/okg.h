@@ -68,8 +68,8 @@ typedef struct okg_params {
                                < 0 = never */
   int32_t disable_pdl;      /* 1: launch without programmatic dependent launch */
   int32_t mg_fuse;          /* temporally blocked V(2,2) level kernels (one "down" and one
-                               "up" launch per level): 0 = default (2D: every level
-                               but the finest; 3D: levels with n <= 32), 1 = every
+                               "up" launch per level): 0 = default (2D: levels but the
+                               finest with n <= 512; 3D: levels with n <= 16), 1 = every
                                level, 2 = every level but the finest, < 0 = never */
   int32_t nslabs;           /* slab decomposition: split the mesh into this
                                many x-plane slabs, one host thread + CUDA stream each;

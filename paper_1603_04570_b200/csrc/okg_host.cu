@@ -2024,12 +2024,14 @@ static void build(okg_ctx* c) {
       tail_dispatch<DIM>(c->lv[c->tail_start].g.n, [&](auto N0) { tail_prepare<DIM, decltype(N0)::value>(c); });
     }
     // temporally blocked down/up kernels for V(2,2) (okg_vcycle.cuh)
-    // default: every coarse level in 2D; in 3D the levels with n <= 32 (the halo-3
-    // redundancy of a 3D box outweighs the saved launches on bigger levels)
+    // default: the coarse levels with n <= 512 in 2D, n <= 16 in 3D; above that the
+    // tiled single sweeps are faster (measured per step: 2D 2048^2 61.1 vs 62.4 ms with
+    // the 1025^2 level tiled; 3D 128^3 49.1 vs 49.3 ms with the 33^3 level tiled --
+    // the halo-3 redundancy of a box outweighs the saved launches on bigger levels)
     // (halo 3 / 2: only on levels that are not split across slabs)
     if (p.mg_pre == 2 && p.mg_post == 2 && p.mg_fuse >= 0)
       for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l)
-        if ((p.mg_fuse >= 1 || DIM == 2 || c->lv[l].g.n <= 32) && c->lv[l].gh == 0 &&
+        if ((p.mg_fuse >= 1 || c->lv[l].g.n <= (DIM == 2 ? 512 : 16)) && c->lv[l].gh == 0 &&
             (c->lv[l].rep || S == 1))
           c->lv[l].fused = true;
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)
