@@ -590,6 +590,7 @@ template <int DIM, int LOAD, int EPI>
 static void tiled(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
   if (L.tl.ichunk == 8) tiled_ti<DIM, LOAD, EPI, 8>(c, L, op, a);
   else if (L.tl.ichunk == 4) tiled_ti<DIM, LOAD, EPI, 4>(c, L, op, a);
+  else if (L.tl.ichunk == 3) tiled_ti<DIM, LOAD, EPI, 3>(c, L, op, a);
   else tiled_ti<DIM, LOAD, EPI, 2>(c, L, op, a);
 }
 
@@ -617,18 +618,13 @@ static void make_tiling(okg_ctx* c, Level& L) {
   t.ci1 = std::min(n, L.g.ihi);
   const int nci = std::max(0, t.ci1 - t.ci0);
   const int base = t.ktiles * t.jtiles;
-  // vertices per thread along x (TI): 8 (the tile is staged by cp.async, no register
-  // staging; the C-block kernels keep 4 in 3D for their register budget); smaller when
-  // the level is too small to give each SM a few CTAs
+  // C-block kernels (okg_tiled_c.cuh): vertices per thread along x 4 in 3D (register
+  // budget), 8 in 2D; smaller when the level is too small to give each SM a few CTAs
   auto chunking = [&](int ichunk, Tiling& tt) {
     while (ichunk > 2 && base * ((nci + ichunk - 1) / ichunk) < 148 * 4) ichunk /= 2;
     tt.ichunk = ichunk;
     tt.ncore = base * ((nci + ichunk - 1) / ichunk);
   };
-#ifndef OKG_FINE_TI
-#define OKG_FINE_TI 8
-#endif
-  chunking(OKG_FINE_TI, t);
   std::vector<uint32_t> bnd;
   const int s = n + 1;
   if (DIM == 3) {
@@ -643,6 +639,27 @@ static void make_tiling(okg_ctx* c, Level& L) {
         if (i == 0 || i == n || k == 0 || k == n) bnd.push_back((uint32_t)(i * s + k));
   }
   t.nbnd = (uint32_t)bnd.size();
+  const int nbb = (int)((t.nbnd + TC::NT - 1) / TC::NT);
+  {
+    // planes per core CTA: the k_tiled grid runs in waves of 148 x 4 CTAs (4 per SM by
+    // registers), and a CTA's time grows like TI + 4 (staging halo + fixed cost), so
+    // take the TI in {8, 4, 3, 2} with the fewest waves x (TI + 4) (ties: larger TI).
+    // Measured against "largest power of two with >= 4 CTAs per SM": 65^3 level TI 2
+    // -> 3 (one wave instead of 609 CTAs on 592 slots), 1025^2 TI 4 -> 8 (one wave):
+    // 3D 128^3 49.1 -> 48.8 ms, 2D 2048^2 61.1 -> 60.5 ms per step, 400^3 unchanged
+    int best = 8;
+    long bestc = -1;
+    for (int ti : {8, 4, 3, 2}) {
+      const long T = (long)base * ((nci + ti - 1) / ti) + nbb;
+      const long cost = ((T + 148 * 4 - 1) / (148 * 4)) * (ti + 4);
+      if (bestc < 0 || cost < bestc) {
+        bestc = cost;
+        best = ti;
+      }
+    }
+    t.ichunk = best;
+    t.ncore = base * ((nci + best - 1) / best);
+  }
   double* d = dalloc(c, (bnd.size() + 1) / 2 + 1);
   CK(cudaMemcpyAsync(d, bnd.data(), bnd.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
   t.bnd = reinterpret_cast<const uint32_t*>(d);
