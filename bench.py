@@ -68,7 +68,7 @@ WEAK_N = {
 
 # dominant kernel for the roofline object (top kernel by share of the step in
 # the committed ncu launch list, profiles/)
-DOMINANT = "smooth"
+DOMINANT = "resid"  # k_tiled<DIM, L_PLAIN, T_RESID, 8>: 12.6 % (3D 128^3) / 16.5 % (400^3) of a step
 
 
 def env_int(k, d):
@@ -362,7 +362,7 @@ def main():
     dom = kernels.get(DOMINANT)
     roofline = None
     if dom:
-        roofline = {"bound": "hbm", "kernel": f"{DOMINANT} (fine-level damped-Jacobi sweep on Shat_0, k_tiled<{dim}, L_PLAIN, T_JACOBI, 8>)",
+        roofline = {"bound": "hbm", "kernel": f"{DOMINANT} (fine-level residual sweep b - Shat_0 x, k_tiled<{dim}, L_PLAIN, T_RESID, 8>)",
                     "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
                     "peak_source": peak_src, "traffic": None,
                     "alg_bytes_per_launch": dom["alg_bytes"], "avg_launch_us": dom["avg_us"]}

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <condition_variable>
 #include <functional>
@@ -134,10 +135,13 @@ struct okg_ctx {
   size_t coarse_ld = 0;
   int coarse_nb = 0;  // > 0: one slab, symmetric packed blocks (k_coarse_sym)
   double *coarse_R = nullptr, *coarse_C = nullptr;
+  unsigned* coarse_cnt = nullptr;  // row-block counters of k_coarse_sym1
   // collapsed bottom of the V-cycle (okg_params.mg_collapse): level collapse_level and
   // everything below it as one symmetric dense operator, packed like the coarse inverse
   int collapse_level = -1, col_nb = 0;
   double *col_A = nullptr, *col_R = nullptr, *col_C = nullptr;
+  unsigned* col_cnt = nullptr;
+  bool coarse1 = false;  // coarse_sym_apply: one launch (env OKG_COARSE1=1) or two
   int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
   int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
   double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
@@ -682,6 +686,25 @@ static void copy(okg_ctx* c, const double* x, double* y, size_t n) {
   CK(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
 }
 
+// y = A x, A symmetric as packed CB-blocks (coarsest inverse / collapsed bottom):
+// two launches (k_coarse_sym, k_coarse_sym_sum), or with OKG_COARSE1=1 in the
+// environment at okg_create one (k_coarse_sym1: the last contributor of a row block
+// sums it) -- same bits, but measured slower (the row sums pile up at the tail of
+// the grid): 128^3 45.0 vs 44.4 ms, 400^3 976 vs 957 ms, 2D 2048^2 56.7 vs 56.5 ms
+static void coarse_sym_apply(okg_ctx* c, int n, int nb, const double* A, const double* x, double* R, double* C,
+                             double* y, unsigned* cnt) {
+  const unsigned nblk = (unsigned)(nb * (nb + 1) / 2);
+  if (c->coarse1) {
+    launch(c, k_coarse_sym1, nblk, 256, 0, n, nb, A, x, R, C, y, cnt);
+    note(c);
+    return;
+  }
+  launch(c, k_coarse_sym, nblk, 256, 0, n, A, x, R, C);
+  note(c);
+  launch(c, k_coarse_sym_sum, (unsigned)nb, CB * CSEG, 0, n, nb, (const double*)R, (const double*)C, y);
+  note(c);
+}
+
 // ---- multigrid (multigrid.hpp:97-149) --------------------------------------
 static void allgather_planes(okg_ctx* c, int l, double* x);
 
@@ -702,12 +725,7 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
   }
   if (c->coarse_nb > 0) {  // one slab: half the bytes through the symmetric block triangle
     const int nb = c->coarse_nb;
-    launch(c, k_coarse_sym, (unsigned)(nb * (nb + 1) / 2), 256, 0, c->nc, (const double*)c->Ainv, b, c->coarse_R,
-           c->coarse_C);
-    note(c);
-    launch(c, k_coarse_sym_sum, (unsigned)nb, CB * CSEG, 0, c->nc, nb, (const double*)c->coarse_R,
-           (const double*)c->coarse_C, y);
-    note(c);
+    coarse_sym_apply(c, c->nc, nb, c->Ainv, b, c->coarse_R, c->coarse_C, y, c->coarse_cnt);
     return;
   }
   double* tgt = c->coarse_split ? L.ea : y;
@@ -748,6 +766,7 @@ static void collapse_levels(okg_ctx* c, int lc) {
     c->col_A = dalloc(c, nblk * CB * CB);
     c->col_R = dalloc(c, nblk * CB);
     c->col_C = dalloc(c, nblk * CB);
+    c->col_cnt = reinterpret_cast<unsigned*>(dalloc(c, nb));  // zeroed
     k_coarse_pack<<<148 * 8, 256, 0, c->stream>>>(N, nb, F, c->col_A);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
@@ -813,6 +832,7 @@ static void coarse_inverse_device(okg_ctx* c, const std::vector<double>& Ad, int
       c->Ainv = dalloc(c, nblk * CB * CB);
       c->coarse_R = dalloc(c, nblk * CB);
       c->coarse_C = dalloc(c, nblk * CB);
+      c->coarse_cnt = reinterpret_cast<unsigned*>(dalloc(c, nb));  // zeroed
       k_coarse_pack<<<148 * 8, 256, 0, c->stream>>>(nc, nb, F, c->Ainv);
       c->coarse_nb = nb;
     } else {
@@ -955,12 +975,7 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   }
   if (l == c->collapse_level && !acc) {  // the whole cycle below l in one matvec
     const int nb = c->col_nb;
-    launch(c, k_coarse_sym, (unsigned)(nb * (nb + 1) / 2), 256, 0, (int)L.g.N, (const double*)c->col_A, rhs, c->col_R,
-           c->col_C);
-    note(c);
-    launch(c, k_coarse_sym_sum, (unsigned)nb, CB * CSEG, 0, (int)L.g.N, nb, (const double*)c->col_R,
-           (const double*)c->col_C, out);
-    note(c);
+    coarse_sym_apply(c, (int)L.g.N, nb, c->col_A, rhs, c->col_R, c->col_C, out, c->col_cnt);
     return;
   }
   if (l == c->tail_start && !acc && l > 0) {
@@ -1902,6 +1917,7 @@ template <int DIM>
 static void build(okg_ctx* c) {
   const okg_params& p = c->p;
   const UnitTables ut = build_unit_tables(DIM);
+  if (const char* e = std::getenv("OKG_COARSE1")) c->coarse1 = std::atoi(e) != 0;
   const int n = p.n;
   c->h = 1.0 / n;
   const double hd = ipow(c->h, DIM), hk = ipow(c->h, DIM - 2);
@@ -2048,7 +2064,7 @@ static void build(okg_ctx* c) {
     // (halo 3 / 2: only on levels that are not split across slabs)
     if (p.mg_pre == 2 && p.mg_post == 2 && p.mg_fuse >= 0)
       for (size_t l = (p.mg_fuse == 1 ? 0 : 1); l + 1 < c->lv.size(); ++l)
-        if ((p.mg_fuse >= 1 || c->lv[l].g.n <= (DIM == 2 ? 512 : 16)) && c->lv[l].gh == 0 &&
+        if ((p.mg_fuse >= 1 || c->lv[l].g.n <= (DIM == 2 ? OKG_MG2_FUSE_N : OKG_MG3_FUSE_N)) && c->lv[l].gh == 0 &&
             (c->lv[l].rep || S == 1))
           c->lv[l].fused = true;
     // shared-memory tiled kernels for the large levels (okg_tiled.cuh)

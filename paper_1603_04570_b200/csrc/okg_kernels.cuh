@@ -334,14 +334,11 @@ __device__ __forceinline__ void tri_index(int b, int& I, int& J) {
   J = b - i * (i + 1) / 2;
 }
 
-__global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __restrict__ Ap,
-                                                    const double* __restrict__ x, double* __restrict__ R,
-                                                    double* __restrict__ Cp) {
-  PDL_ENTRY();
+// one block (I, J) of the packed triangle: R(I,J) = A_IJ x_J, C(I,J) = A_IJ^T x_I
+__device__ __forceinline__ void coarse_sym_block(int nc, const double* __restrict__ Ap, const double* __restrict__ x,
+                                                 double* __restrict__ R, double* __restrict__ Cp, int I, int J) {
   __shared__ double xs_i[CB], xs_j[CB];
   __shared__ double cpart[8][CB];
-  int I, J;
-  tri_index(blockIdx.x, I, J);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid < CB) {
     const int r = I * CB + tid, c = J * CB + tid;
@@ -366,7 +363,7 @@ __global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __rest
     c0 = fma(a[q].x, xr, c0);
     c1 = fma(a[q].y, xr, c1);
   }
-  if (I == J) return;
+  if (I == J) return;  // (CTA-uniform)
   cpart[w][2 * lane] = c0;
   cpart[w][2 * lane + 1] = c1;
   __syncthreads();
@@ -378,20 +375,33 @@ __global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __rest
   }
 }
 
+__global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __restrict__ Ap,
+                                                    const double* __restrict__ x, double* __restrict__ R,
+                                                    double* __restrict__ Cp) {
+  PDL_ENTRY();
+  int I, J;
+  tri_index(blockIdx.x, I, J);
+  coarse_sym_block(nc, Ap, x, R, Cp, I, J);
+}
+
 // y_r (r in block I) = sum_{J <= I} R(I,J)_r + sum_{K > I} C(K,I)_r.  The nb terms
 // of a row are split into SEG contiguous segments (one warp-row of threads each,
 // loads issued 4 at a time), the segment sums then added in segment order: a fixed
 // order, so the result is deterministic.
 constexpr int CSEG = 4;
-__global__ void __launch_bounds__(CB * CSEG) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
-                                                              const double* __restrict__ Cp, double* __restrict__ y) {
-  PDL_ENTRY();
+// rows of block I (blockDim = CB * CSEG); COHERENT: the partials were written by other
+// CTAs of the running grid (k_coarse_sym1), so they are read through L2, not the
+// non-coherent path
+template <bool COHERENT>
+__device__ __forceinline__ void coarse_sym_rows(int nc, int nb, const double* __restrict__ R,
+                                                const double* __restrict__ Cp, double* __restrict__ y, int I) {
   __shared__ double part[CSEG][CB];
-  const int I = blockIdx.x, t = threadIdx.x % CB, sg = threadIdx.x / CB;
+  const int t = threadIdx.x % CB, sg = threadIdx.x / CB;
   const size_t base = (size_t)I * (I + 1) / 2;
+  auto ld = [](const double* p) -> double { return COHERENT ? __ldcg(p) : __ldg(p); };
   // term q (0..nb-1): q <= I -> R(I, q), else C(q, I)
   auto term = [&](int q) -> double {
-    return q <= I ? __ldg(R + (base + q) * CB + t) : __ldg(Cp + ((size_t)q * (q + 1) / 2 + I) * CB + t);
+    return q <= I ? ld(R + (base + q) * CB + t) : ld(Cp + ((size_t)q * (q + 1) / 2 + I) * CB + t);
   };
   const int per = (nb + CSEG - 1) / CSEG, q0 = sg * per, q1 = min(nb, q0 + per);
   double s = 0.0;
@@ -411,6 +421,44 @@ __global__ void __launch_bounds__(CB * CSEG) k_coarse_sym_sum(int nc, int nb, co
 #pragma unroll
     for (int g = 1; g < CSEG; ++g) r += part[g][t];
     if (I * CB + t < nc) y[I * CB + t] = r;
+  }
+}
+
+__global__ void __launch_bounds__(CB * CSEG) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
+                                                              const double* __restrict__ Cp, double* __restrict__ y) {
+  PDL_ENTRY();
+  coarse_sym_rows<false>(nc, nb, R, Cp, y, blockIdx.x);
+}
+
+// k_coarse_sym + k_coarse_sym_sum in one launch: every CTA counts its block into the
+// row blocks it feeds (I and, off the diagonal, J); the CTA that completes a row
+// block (nb contributions) sums it, in k_coarse_sym_sum's order (bit-identical), and
+// re-arms the counter for the next call.  cnt: nb zeroed counters.
+static_assert(CB * CSEG == 256, "k_coarse_sym1 runs both halves with one block shape");
+__global__ void __launch_bounds__(256) k_coarse_sym1(int nc, int nb, const double* __restrict__ Ap,
+                                                     const double* __restrict__ x, double* __restrict__ R,
+                                                     double* __restrict__ Cp, double* __restrict__ y,
+                                                     unsigned* __restrict__ cnt) {
+  PDL_ENTRY();
+  __shared__ int fin[2];
+  int I, J;
+  tri_index(blockIdx.x, I, J);
+  coarse_sym_block(nc, Ap, x, R, Cp, I, J);
+  __threadfence();  // this CTA's partials are visible before it is counted
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fin[0] = atomicAdd(cnt + I, 1u) == (unsigned)nb - 1 ? I : -1;
+    fin[1] = (I != J && atomicAdd(cnt + J, 1u) == (unsigned)nb - 1) ? J : -1;
+    __threadfence();
+  }
+  __syncthreads();
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int rb = fin[f];
+    if (rb < 0) continue;  // (CTA-uniform)
+    coarse_sym_rows<true>(nc, nb, R, Cp, y, rb);
+    if (threadIdx.x == 0) cnt[rb] = 0u;
+    __syncthreads();  // part[] reuse
   }
 }
 

@@ -22,17 +22,34 @@ namespace okg {
 // larger box used on big levels (less halo redundancy, fewer CTAs)
 template <int DIM, int BX = 0>
 struct MgBox;
+#ifndef OKG_MG3_FI  // (-D overrides: box-shape experiments)
+#define OKG_MG3_FI 2
+#define OKG_MG3_FJ 2
+#define OKG_MG3_FK 8
+#define OKG_MG3_NT 512
+#endif
+#ifndef OKG_MG3_FUSE_N  // 3D / 2D levels with n <= this use the fused kernels (okg_host.cu build)
+#define OKG_MG3_FUSE_N 16
+#endif
+#ifndef OKG_MG2_FUSE_N
+#define OKG_MG2_FUSE_N 512
+#endif
 template <>
 struct MgBox<3, 0> {
-  static constexpr int FI = 4, FJ = 4, FK = 16, NT = 256;
+  static constexpr int FI = OKG_MG3_FI, FJ = OKG_MG3_FJ, FK = OKG_MG3_FK, NT = OKG_MG3_NT;
 };
 template <>
 struct MgBox<3, 1> {
   static constexpr int FI = 4, FJ = 8, FK = 32, NT = 256;
 };
+#ifndef OKG_MG2_FI
+#define OKG_MG2_FI 8
+#define OKG_MG2_FK 16
+#define OKG_MG2_NT 256
+#endif
 template <>
 struct MgBox<2, 0> {
-  static constexpr int FI = 8, FJ = 1, FK = 64, NT = 256;
+  static constexpr int FI = OKG_MG2_FI, FJ = 1, FK = OKG_MG2_FK, NT = OKG_MG2_NT;
 };
 template <>
 struct MgBox<2, 1> {
