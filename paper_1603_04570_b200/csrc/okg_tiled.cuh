@@ -49,6 +49,9 @@ struct Tiling {
 };
 
 enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2 };
+#ifndef OKG_JAC0_FOLD  // inner JAC0 tiles: scale folded into the taps (see k_tiled)
+#define OKG_JAC0_FOLD 1
+#endif
 enum TEpi {
   T_APPLY = 0,       // y = A s
   T_RESID = 1,       // y = b - A s
@@ -251,13 +254,20 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   const bool active = k <= g.n - 1 && (DIM == 2 || j <= g.n - 1);
   const uint32_t idx0 = DIM == 3 ? (uint32_t)i0 * g.ps + (uint32_t)j * g.s + k : (uint32_t)i0 * g.s + k;
   const uint32_t pstride = DIM == 3 ? g.ps : (uint32_t)g.s;
+  // JAC0 on a tile whose halo holds no boundary vertex: one constant scale w D^-1,
+  // FOLDED into the taps (x' = wd * x rounds exactly like the staging transform, so
+  // the bits are the same) -- the tile keeps the raw rhs, which is also the
+  // epilogue's b (a.x == a.b): no transform pass and no prefetch of b
+  const bool inner = i0 - 1 >= 1 && i0 + ni <= g.n - 1 && k0 - 1 >= 1 && k0 + TC::TK <= g.n - 1 &&
+                     (DIM == 2 || (j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1));
+  const bool fold = OKG_JAC0_FOLD && LOAD == L_JAC0 && inner && a.x == a.b;
   // prefetch the pointwise operands of this thread's TI vertices
   double pb[TI], pp[TI];
 #pragma unroll
   for (int t = 0; t < TI; ++t) {
     const bool ok = active && t < ni;
     const uint32_t idx = idx0 + (uint32_t)t * pstride;
-    pb[t] = (EpiNeeds<EPI>::B && ok) ? a.b[idx] : 0.0;
+    pb[t] = (EpiNeeds<EPI>::B && ok && !fold) ? a.b[idx] : 0.0;
     pp[t] = (EpiNeeds<EPI>::P2 && ok) ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx]) : 0.0;
   }
   // L_PROLONG: coarse tile covering the fine planes/rows/columns of the staged tile
@@ -350,11 +360,10 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     // staging transform:  L_JAC0 r -> (w D^-1) r ;
     //                     L_PROLONG e -> e + P e_c  (x + t, multigrid.hpp:111-112)
     constexpr int CSI = CT::CJ * CT::CK, CSJ = CT::CK;
-    // JAC0 on a tile whose halo holds no boundary vertex: one constant scale
-    const bool inner = i0 - 1 >= 1 && i0 + ni <= g.n - 1 && k0 - 1 >= 1 && k0 + TC::TK <= g.n - 1 &&
-                       (DIM == 2 || (j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1));
     const double wd = a.omega * op.invd;
-    if (LOAD == L_JAC0 && inner) {
+    if (fold) {
+      // (scale applied in the taps below)
+    } else if (LOAD == L_JAC0 && inner) {
       // branch-free: every slot of this thread (out-of-box / unused slots are never read)
 #pragma unroll
       for (int p = 0; p < TI + 2; ++p)
@@ -421,19 +430,26 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   if (!active) return;
   // all TI vertex chains are computed unconditionally (no branch between them, so
   // their dependent FMA chains interleave); only the stores are predicated
+  // JAC0: taps scaled by scl (wd on folded tiles, else 1.0 -- exact)
+  const double scl = fold ? a.omega * op.invd : 1.0;
 #pragma unroll
   for (int t = 0; t < TI; ++t) {
-    double As = 0.0, s_own = 0.0;
+    double As = 0.0, s_own = 0.0, raw_own = 0.0;
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
       const int di = off_comp(DIM, o, 0);
       const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
       const int dk = off_comp(DIM, o, DIM - 1);
-      const double sv = tile[(t + 1 + di) * TC::PSZ + (DIM == 3 ? (tj + 1 + dj) * TC::PW : 0) + tk + 1 + dk];
-      if (o == Traits<DIM>::CENTER) s_own = sv;
+      const double raw = tile[(t + 1 + di) * TC::PSZ + (DIM == 3 ? (tj + 1 + dj) * TC::PW : 0) + tk + 1 + dk];
+      const double sv = (OKG_JAC0_FOLD && LOAD == L_JAC0) ? scl * raw : raw;
+      if (o == Traits<DIM>::CENTER) {
+        s_own = sv;
+        raw_own = raw;
+      }
       As = fma(op.w[o], sv, As);
     }
-    if (t < ni) epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, pb[t], pp[t]);
+    if (t < ni)
+      epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, fold ? raw_own : pb[t], pp[t]);
   }
 }
 
