@@ -14,8 +14,24 @@ stream, bracketed by barrier + synchronize.  value = sum(2N * newton_iters) /
 time.  The per-step working set (31 Krylov vectors of 2N doubles = 1.1 GB)
 is far larger than the 126 MB L2, so no explicit flush is needed.
 
+--gpus N > 1 without WORLD_SIZE in the environment re-launches this script
+under torchrun (one process per GPU, 127.0.0.1 rendezvous).  configs[3]
+(c4_3d128, the default) is the SAME 128^3 problem on 1/2/4/8 GPUs (strong
+scaling, x-plane slabs); configs[4] (c5_3d800) grows the mesh with N (weak).
+
 --impl reference times the reference's own CPU newton_solve (oracle/_ref, the
-unmodified okflow headers compiled by oracle/Makefile) on a bounded sample.
+unmodified okflow headers compiled by oracle/Makefile) on the SAME workload
+(setup untimed, then its first timestep timed by the reference's own
+stats.seconds): one instance alone (one host core), then as many concurrent
+single-threaded instances as host cores and RAM allow (the value: the box's
+whole CPU).
+
+Per-kernel numbers (`kernels`, `roofline`): every fine-level kernel is timed
+(a) in-step -- CUPTI activity records (torch.profiler) of one extra timestep
+after the timed region, the launch with the largest grid of that kernel's
+template (the fine level); `roofline.achieved` uses this time -- and (b) alone
+and L2-cold with CUDA events (okg_kernel_timing_ex: a 2 x L2 scratch write
+before every launch, no PDL).
 """
 import argparse
 import json
@@ -66,9 +82,12 @@ WEAK_N = {
     "c5_3d800": {1: 400, 2: 512, 4: 640, 8: 800},      # 64.5M, 67.4M, 65.8M, 64.2M vertices per GPU
 }
 
-# dominant kernel for the roofline object (top kernel by share of the step in
-# the committed ncu launch list, profiles/)
-DOMINANT = "resid"  # k_tiled<DIM, L_PLAIN, T_RESID, 8>: 12.6 % (3D 128^3) / 16.5 % (400^3) of a step
+# N > 1 default: configs[3] is the same 128^3 problem on 2/4/8 GPUs (strong);
+# configs[4] is weak-scaled (100^3 cells per GPU-equivalent share)
+DEFAULT_SCALING = {"c4_3d128": "strong", "c2_2d2048": "strong", "c1_2d64": "strong", "c5_3d800": "weak"}
+
+# (the roofline kernel is chosen live: the fine-level kernel with the largest share
+#  of the in-step device time)
 
 
 def env_int(k, d):
@@ -131,57 +150,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference(dim, n, eps, m, seed, steps, warmup, budget_s=None):
-    """The reference's own newton_solve (oracle/_ref) on one host core."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle as po
-    kind = "ref" if po.available("ref") else "port"
-    p = po.baseline_params(dim, n, eps=eps, m=m, kind=kind)
-    o = po.Oracle(p, kind)
-    u0 = po.seeded_ic(o.n, seed, m, kind)
-    w0 = np.zeros(o.n)
-    u, w = u0, w0
-    for _ in range(warmup):
-        u, w, _ = o.newton_solve(u, w)
-    u, w = u0, w0
-    secs, dofs, iters = 0.0, 0, []
-    t_start = time.time()
-    for k in range(steps):
-        u, w, st = o.newton_solve(u, w)
-        secs += st.seconds
-        dofs += 2 * o.n * st.newton_iters
-        iters.append(st.gmres_iters)
-        if budget_s is not None and k >= 1 and time.time() - t_start > budget_s:
-            break
-    return {"value": dofs / secs, "seconds": secs, "steps": len(iters), "gmres_iters": iters,
-            "kind": "reference" if kind == "ref" else "port", "N": o.n,
-            "cpu": _cpu_model(), "nproc": os.cpu_count()}
-
-
-def _ref_worker(args):
-    dim, n, eps, m, seed, steps, warmup, budget_s = args
-    return cpu_reference(dim, n, eps, m, seed, steps, warmup, budget_s)
-
-
-def cpu_reference_all_cores(dim, n, eps, m, seed, steps, warmup, budget_s=None, procs=None):
-    """The reference's newton_solve on every host core: it is single-threaded
-    (proj/README.md:182-184), so the box's CPU throughput is `procs` independent
-    solver instances running concurrently (one process each, same sample); the
-    aggregate DoF/s is the sum of the instances' rates, each timed by the
-    reference's own stats.seconds while all run."""
-    import multiprocessing as mp
-    procs = procs or os.cpu_count() or 1
-    with mp.get_context("spawn").Pool(procs) as pool:
-        rs = pool.map(_ref_worker, [(dim, n, eps, m, seed, steps, warmup, budget_s)] * procs)
-    r = dict(rs[0])
-    r["value"] = sum(x["value"] for x in rs)
-    r["per_core"] = [x["value"] for x in rs]
-    r["procs"] = procs
-    r["steps"] = min(x["steps"] for x in rs)
-    r["seconds"] = max(x["seconds"] for x in rs)
-    return r
-
-
 def _cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -192,29 +160,168 @@ def _cpu_model():
     return "unknown"
 
 
+def _mem_available():
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+# peak RSS of one reference instance per vertex (7.19 GB at 3D 128^3,
+# 4.68 GB at 2D 2048^2), rounded up
+REF_BYTES_PER_VERTEX = {2: 1200, 3: 3600}
+
+
+def ref_instance(args):
+    """One reference instance (oracle/_ref: the unmodified okflow headers): build_mesh +
+    assemble_operators + make_schur_context (untimed), then newton_solve timesteps from
+    the seeded IC until `budget_s` of solve time (at least one), each timed by the
+    reference's own stats.seconds (model.hpp:168,211-213)."""
+    dim, n, eps, m, seed, min_coarse, budget_s, max_steps = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    kind = "ref" if po.available("ref") else "port"
+    t0 = time.time()
+    p = po.baseline_params(dim, n, eps=eps, m=m, kind=kind, min_coarse_size=min_coarse)
+    o = po.Oracle(p, kind)
+    setup_s = time.time() - t0
+    u = po.seeded_ic(o.n, seed, m, kind)
+    w = np.zeros(o.n)
+    secs, dofs, iters = 0.0, 0, []
+    while True:
+        u, w, st = o.newton_solve(u, w)
+        secs += st.seconds
+        dofs += 2 * o.n * st.newton_iters
+        iters.append(st.gmres_iters)
+        if secs >= budget_s or len(iters) >= max_steps:
+            break
+    o.close()
+    return {"value": dofs / secs, "seconds": secs, "steps": len(iters), "gmres_iters": iters,
+            "kind": "reference" if kind == "ref" else "port", "N": int(o.n), "setup_s": setup_s}
+
+
+def ref_concurrent(dim, n, eps, m, seed, min_coarse, budget_s, max_steps, procs):
+    """`procs` single-threaded reference instances at once (one process each): the
+    reference has no threading (proj/README.md:182-184), so this is the box's whole
+    CPU.  Aggregate = sum of the instances' rates."""
+    import multiprocessing as mp
+    a = (dim, n, eps, m, seed, min_coarse, budget_s, max_steps)
+    with mp.get_context("spawn").Pool(procs) as pool:
+        rs = pool.map(ref_instance, [a] * procs)
+    return {"value": sum(x["value"] for x in rs), "per_instance": [x["value"] for x in rs], "procs": procs,
+            "steps": min(x["steps"] for x in rs), "seconds": max(x["seconds"] for x in rs),
+            "gmres_iters": rs[0]["gmres_iters"], "kind": rs[0]["kind"], "N": rs[0]["N"],
+            "setup_s": max(x["setup_s"] for x in rs)}
+
+
+def workload_mesh(workload, world, scaling):
+    dim, n, eps, m, seed, n_cpu, desc = WORKLOADS[workload]
+    if (world > 1 and scaling == "weak") or (world == 1 and workload == "c5_3d800"):
+        n = WEAK_N[workload].get(world)
+        if n is None:
+            raise SystemExit(f"--scaling weak: no mesh for {world} GPUs (have {sorted(WEAK_N[workload])})")
+    return dim, n
+
+
+def workload_config(workload, dim, n):
+    """The workload's config object -- identical in both arms (GPU and --impl reference)."""
+    N = (n + 1) ** dim
+    return {"workload": workload, "description": WORKLOADS[workload][6], "dim": dim, "n": n, "dofs": 2 * N,
+            "l2": f"inputs larger than L2: per-step working set ({31 * 2 * N * 8 / 1e9:.2f} GB Krylov basis "
+                  f"+ level vectors) >> 126 MB L2; no flush"}
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    dim, n, eps, m, seed, n_cpu, desc = WORKLOADS[args.workload]
-    r = cpu_reference_all_cores(dim, n_cpu, eps, m, seed, args.steps, args.warmup)
-    sample = (f"{dim}D {n_cpu}^{dim} (same parameters, {r['N']} vertices), {r['steps']} timesteps of the "
-              f"reference newton_solve after {args.warmup} warm-up steps, in {r['procs']} concurrent "
-              f"single-threaded instances (the reference has no threading, proj/README.md:182-184; one "
-              f"instance per host core, aggregate = sum of their rates; per instance "
-              f"{min(r['per_core']):.3g}-{max(r['per_core']):.3g} DoF/s); CPU {r['cpu']}, nproc {r['nproc']}")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "DoF/s", "n_gpus": world,
-        "steps": r["steps"], "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / r["steps"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded IC, SURVEY.md 8(d))",
-        "config": {"workload": args.workload, "description": desc, "sample_n": n_cpu},
-        "cpu_baseline": {"value": r["value"], "unit": "DoF/s", "cores": r["procs"], "kind": r["kind"],
-                         "sample": sample},
+    dim, _, eps, m, seed, _, desc = WORKLOADS[args.workload]
+    dim, n = workload_mesh(args.workload, world, args.scaling)
+    cfg = workload_config(args.workload, dim, n)
+    base = {"impl": "reference", "metric": METRIC, "unit": "DoF/s", "n_gpus": world, "config": cfg}
+    if args.workload == "c5_3d800":
+        base["unavailable"] = ("the reference cannot run configs[4]: its coarsest 26^3 = 17,576 exceeds the "
+                               "dense cap (ConfigError, multigrid.hpp:52,67-71); with the cap raised its host "
+                               "Cholesky of 17,576^2 and int32 CSR put it at hours per step")
+        print(json.dumps(base), flush=True)
+        return 0
+    N = (n + 1) ** dim
+    need = REF_BYTES_PER_VERTEX[dim] * N + (256 << 20)
+    ncpu = os.cpu_count() or 1
+    procs = max(1, min(ncpu, int(0.85 * _mem_available() // need) if _mem_available() else 1))
+    if args.ref_procs:
+        procs = args.ref_procs
+    a = (dim, n, eps, m, seed, MIN_COARSE.get(args.workload, 500), args.ref_budget, max(1, args.steps))
+    single = None
+    if world == 1 and not args.ref_no_single:
+        single = ref_instance(a)
+    r = ref_concurrent(*a, procs)
+    cpu = _cpu_model()
+    sample = (f"the workload itself ({dim}D {n}^{dim}, {N} vertices): setup untimed, then the first "
+              f"{r['steps']} timestep(s) of the reference newton_solve from the seeded IC, timed by its own "
+              f"stats.seconds, in {procs} concurrent single-threaded instances (the reference has no threading, "
+              f"proj/README.md:182-184; {procs} = min(nproc {ncpu}, 85% of MemAvailable / "
+              f"{need / 1e9:.1f} GB per instance)); aggregate = sum of the instances' rates, per instance "
+              f"{min(r['per_instance']):.3g}-{max(r['per_instance']):.3g} DoF/s; CPU {cpu}")
+    line = dict(base)
+    line.update({
+        "value": r["value"], "steps": r["steps"], "warmup": 0,
+        "warmup_note": "no warm-up timestep: compiled C++ with no JIT or caches to prime; the untimed setup "
+                       "(assembly + Schur context) touches the whole working set first",
+        "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
+        "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded IC u0 = m + 0.01 U(-1,1), SURVEY.md 8(d); no dataset involved)",
+        "parallelism": f"{procs} concurrent single-threaded instances on the host CPU",
+        "cpu_baseline": {"value": r["value"], "unit": "DoF/s", "cores": procs, "kind": r["kind"], "sample": sample},
         "e2e": {"value": r["value"], "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gmres_iters": r["gmres_iters"],
-    }
+        "gmres_iters": r["gmres_iters"], "setup_s": r["setup_s"],
+    })
+    if single is not None:
+        line["single_instance"] = {
+            "value": single["value"], "unit": "DoF/s", "cores": 1, "steps": single["steps"],
+            "seconds": single["seconds"], "setup_s": single["setup_s"], "gmres_iters": single["gmres_iters"],
+            "sample": "one instance alone on the idle host (one core), same workload and timing as above"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# in-step kernel timing: the fine-level launch of each okg_kernel_timing id, matched by
+# kernel template (demangled name prefix) and the largest grid of that template
+def _kt_prefixes(dim):
+    t = f"okg::k_tiled<{dim}, "
+    return {"smooth": t + "0, 2,", "resid": t + "0, 1,", "pre2": t + "1, 2,", "post_acc": t + "0, 4,",
+            "cheb": t + "0, 5,", "jacobian": f"okg::k_tiled_c<{dim}, 5,", "restrict": f"okg::k_restrict<{dim}>",
+            "prolong": t + "2, 2,"}
+
+
+def instep_profile(ctx, torch):
+    """CUPTI activity records (torch.profiler/kineto) of ONE extra timestep after the
+    timed region: per (kernel, grid) the launch count and device time."""
+    import tempfile
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        ctx.step_resident()
+        torch.cuda.synchronize()
+    fd, path = tempfile.mkstemp(suffix=".json")
+    os.close(fd)
+    try:
+        prof.export_chrome_trace(path)
+        tr = json.load(open(path))
+    finally:
+        os.unlink(path)
+    agg, total = {}, 0.0
+    for ev in tr.get("traceEvents", []):
+        if ev.get("cat") != "kernel":
+            continue
+        grid = tuple(ev.get("args", {}).get("grid", (0, 0, 0)))
+        d = agg.setdefault((ev["name"], grid), {"n": 0, "us": 0.0})
+        d["n"] += 1
+        d["us"] += float(ev.get("dur", 0.0))
+        total += float(ev.get("dur", 0.0))
+    return agg, total
 
 
 def main():
@@ -226,15 +333,36 @@ def main():
     ap.add_argument("--workload", default="c4_3d128", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of reference CPU work (cpu_baseline)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = mesh grows with N (WEAK_N), strong = the workload's mesh split N ways")
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="--impl reference: seconds of timed newton_solve per instance (at least one timestep)")
+    ap.add_argument("--ref-procs", type=int, default=0, help="--impl reference: concurrent instances (0: auto)")
+    ap.add_argument("--ref-no-single", action="store_true", help="--impl reference: skip the one-instance run")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: weak = mesh grows with N (WEAK_N), strong = the workload's mesh split N ways "
+                         "(default per workload: configs[3] strong, configs[4] weak)")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel timings")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.scaling is None:
+        args.scaling = DEFAULT_SCALING.get(args.workload, "strong")
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (127.0.0.1 rendezvous)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
 
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU "
+                         f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
@@ -242,6 +370,7 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (rank / nranks) on stderr
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     device = local_rank if world > 1 else 0
@@ -250,11 +379,8 @@ def main():
     from paper_1603_04570_b200 import _lib
     import ctypes as C
 
-    dim, n, eps, m, seed, n_cpu, desc = WORKLOADS[args.workload]
-    if (world > 1 and args.scaling == "weak") or (world == 1 and args.workload == "c5_3d800"):
-        n = WEAK_N[args.workload].get(world)
-        if n is None:
-            raise SystemExit(f"--scaling weak: no mesh for {world} GPUs (have {sorted(WEAK_N[args.workload])})")
+    _, _, eps, m, seed, n_cpu, desc = WORKLOADS[args.workload]
+    dim, n = workload_mesh(args.workload, world, args.scaling)
     cfg = okg.SolverConfig(dim=dim, n=n, eps=eps, m=m, sigma=100.0, theta=0.5, dt=eps * eps,
                            newton_tol=1e-8, gmres_tol=1e-10, gmres_restart=30,
                            min_coarse_size=MIN_COARSE.get(args.workload, 500))
@@ -266,6 +392,8 @@ def main():
             idt.copy_(torch.frombuffer(bytearray(okg.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(idt, 0)
         ctx = okg.SchurContext(cfg, device=device, rank=rank, nranks=world, nccl_id=bytes(idt.cpu().numpy()))
+        print(f"okg: rank {rank} of nranks {world}: solver NCCL communicator initialised on cuda:{device}, "
+              f"x-planes per rank {ctx.slab_planes}", file=sys.stderr, flush=True)
     else:
         ctx = okg.SchurContext(cfg, device=device)
     setup_s = time.time() - t0
@@ -341,7 +469,7 @@ def main():
         dist.all_reduce(lt)  # kernels of every rank
     launches = int(lt.item())
 
-    # ---- per-kernel live timing (CUDA events on the solver stream) ----
+    # ---- per-kernel timing: in-step (CUPTI) and alone L2-cold (CUDA events) ----
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(peaks_path):
@@ -350,41 +478,66 @@ def main():
             peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
         except Exception:
             pass
-    kernels = {}
-    ctx.linearize(u0)
-    for kid, name in enumerate(_lib.KT_NAMES):
-        ms, by = C.c_double(), C.c_double()
-        st = _lib.lib.okg_kernel_timing(ctx.handle, kid, 50, C.byref(ms), C.byref(by))
-        if st == 0:
-            kernels[name] = {"avg_us": ms.value * 1e3, "alg_bytes": by.value,
-                             "gbs": by.value / (ms.value * 1e-3) / 1e9}
-    ctx.clear_linearization()
-    dom = kernels.get(DOMINANT)
-    roofline = None
-    if dom:
-        roofline = {"bound": "hbm", "kernel": f"{DOMINANT} (fine-level residual sweep b - Shat_0 x, k_tiled<{dim}, L_PLAIN, T_RESID, 8>)",
-                    "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
-                    "peak_source": peak_src, "traffic": None,
-                    "alg_bytes_per_launch": dom["alg_bytes"], "avg_launch_us": dom["avg_us"]}
-        prof = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(prof):
-            try:
-                tr = json.load(open(prof)).get(args.workload, {}).get(DOMINANT)
-                if tr:
-                    roofline["traffic"] = tr
-            except Exception:
-                pass
+    kernels, roofline, step_kernel_us = {}, None, None
+    if not args.no_kernels:
+        try:
+            ctx.set_state(ic)
+            agg, step_kernel_us = instep_profile(ctx, torch)
+        except Exception as e:  # report, never fail the GPU line
+            agg, step_kernel_us = {}, None
+            print(f"bench.py: in-step profile failed: {e}", file=sys.stderr)
+        pre = _kt_prefixes(dim)
+        ctx.linearize(u0)
+        for kid, name in enumerate(_lib.KT_NAMES):
+            ms, by = C.c_double(), C.c_double()
+            ent = {}
+            if _lib.lib.okg_kernel_timing_ex(ctx.handle, kid, 20, _lib.KT_COLD | _lib.KT_NO_PDL,
+                                             C.byref(ms), C.byref(by)) == 0:
+                ent = {"alg_bytes": by.value, "cold_us": ms.value * 1e3,
+                       "cold_gbs": by.value / (ms.value * 1e-3) / 1e9}
+            cand = [(k, d) for k, d in agg.items() if k[0].startswith("void " + pre[name])]
+            if cand and ent:
+                (kname, grid), d = max(cand, key=lambda kd: kd[0][1][0] * kd[0][1][1] * kd[0][1][2])
+                avg = d["us"] / d["n"]
+                ent.update({"kernel": kname.split("(")[0].replace("void ", ""), "grid": list(grid),
+                            "instep_n": d["n"], "instep_us": avg,
+                            "instep_gbs": ent["alg_bytes"] / (avg * 1e-6) / 1e9,
+                            "share_of_step": d["us"] / step_kernel_us if step_kernel_us else None})
+            if ent:
+                kernels[name] = ent
+        ctx.clear_linearization()
+        ranked = sorted((k for k in kernels if "share_of_step" in kernels[k]),
+                        key=lambda k: -kernels[k]["share_of_step"])
+        if ranked:
+            dom, d = ranked[0], kernels[ranked[0]]
+            roofline = {"bound": "hbm", "kernel": f"{dom} ({d['kernel']}, grid {d['grid'][0]})",
+                        "achieved": d["instep_gbs"], "peak": peak, "unit": "GB/s", "frac": d["instep_gbs"] / peak,
+                        "peak_source": peak_src, "traffic": None,
+                        "timing": ("in-step: mean device time of this kernel's launches during one timestep "
+                                   "(CUPTI activity records via torch.profiler, one extra step after the "
+                                   "timed region); cold_us = alone, L2 flushed before every launch, no PDL"),
+                        "alg_bytes_per_launch": d["alg_bytes"], "avg_launch_us": d["instep_us"],
+                        "share_of_step": d["share_of_step"], "cold_us": d["cold_us"],
+                        "cold_frac": d["cold_gbs"] / peak}
+            prof = os.path.join(ROOT, "profiles", "traffic.json")
+            if os.path.exists(prof):
+                try:
+                    tr = json.load(open(prof)).get(args.workload, {}).get(dom)
+                    if tr:
+                        roofline["traffic"] = tr
+                except Exception:
+                    pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_all_cores(dim, n_cpu, eps, m, seed, 100, 0, budget_s=args.cpu_budget)
-            cpu = {"value": r["value"], "unit": "DoF/s", "cores": r["procs"], "kind": r["kind"],
-                   "sample": (f"{dim}D {n_cpu}^{dim} ({r['N']} vertices), >= {r['steps']} timesteps of the "
-                              f"reference newton_solve from the same seeded IC in each of {r['procs']} concurrent "
-                              f"single-threaded instances (one per host core; the reference has no threading), "
-                              f"each timed by its own stats.seconds, aggregate = sum of rates; CPU {r['cpu']}, "
-                              f"nproc {r['nproc']}")}
+            r = ref_instance((dim, n_cpu, eps, m, seed, 500, args.cpu_budget, 100))
+            cpu = {"value": r["value"], "unit": "DoF/s", "cores": 1, "kind": r["kind"],
+                   "sample": (f"reduced size: {dim}D {n_cpu}^{dim} ({r['N']} vertices; the workload's own "
+                              f"{n}^{dim} needs minutes of reference setup + solve per timestep, timed by "
+                              f"bench.py --impl reference), same parameters and seeded IC, the first "
+                              f"{r['steps']} timesteps of the reference newton_solve on one host core, timed "
+                              f"by its own stats.seconds; CPU {_cpu_model()}, nproc {os.cpu_count()}")}
         except Exception as e:  # report, never fail the GPU line
             cpu = {"value": None, "unit": "DoF/s", "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -394,12 +547,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps, "higher_is_better": True,
             "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded IC u0 = m + 0.01 U(-1,1), SURVEY.md 8(d); no dataset involved)",
-            "config": {"workload": args.workload, "description": desc, "dim": dim, "n": n, "dofs": 2 * N,
-                       "parallelism": "1 GPU" if world == 1 else
-                       (f"{world} x-plane slabs, one per GPU/process; ghost planes by NCCL send/recv, "
-                        f"Krylov sums by NCCL allreduce; planes per rank {ctx.slab_planes}"),
-                       "l2": f"per-step working set ({31 * 2 * N * 8 / 1e9:.1f} GB Krylov basis) >> 126 MB L2; no flush",
-                       "setup_s": setup_s, "levels": ctx.level_sizes},
+            "config": workload_config(args.workload, dim, n),
+            "parallelism": "1 GPU" if world == 1 else
+                           (f"{world} x-plane slabs, one per GPU/process; ghost planes by NCCL send/recv, "
+                            f"Krylov sums by NCCL allreduce; planes per rank {ctx.slab_planes}"),
+            "setup_s": setup_s, "levels": ctx.level_sizes,
             "newton_iters": [s.newton_iters for s in stats],
             "gmres_iters": [s.gmres_iters for s in stats],
             "clocks": clocks_info,
@@ -408,6 +560,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roofline,
             "kernels": kernels,
+            "step_kernel_us": step_kernel_us,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -249,6 +249,19 @@ int okg_residual_host(okg_ctx* ctx, const double* u_next, const double* w_next,
                       const double* u_old, const double* w_old, double* r1, double* r2);
 int okg_gmres_host(okg_ctx* ctx, const double* b, double* x, double rel_tol, int32_t max_iter,
                    int32_t restart, okg_krylov_stats* stats);
+/* the same four with the caller's array lengths checked first (OKG_EINVAL on a
+ * mismatch, nothing read or written): nx/ny = vertex counts of the kind's input /
+ * output (N, 2N for BLOCK/JACOBIAN, a level size for SHAT/VCYCLE/PROLONG/RESTRICT/
+ * COARSE_SOLVE), n = N (linearize, residual) or 2N (gmres).  Replaces the reference's
+ * dimension checks: LinearOperator::apply (operator.hpp:22-25), gmres
+ * (krylov.hpp:48-51), residual (model.hpp:126-127). */
+int okg_apply_host_n(okg_ctx* ctx, int32_t kind, int32_t level, const double* x, int64_t nx, double* y,
+                     int64_t ny);
+int okg_linearize_host_n(okg_ctx* ctx, const double* u, int64_t n);
+int okg_residual_host_n(okg_ctx* ctx, const double* u_next, const double* w_next, const double* u_old,
+                        const double* w_old, int64_t n, double* r1, double* r2);
+int okg_gmres_host_n(okg_ctx* ctx, const double* b, double* x, int64_t n, double rel_tol, int32_t max_iter,
+                     int32_t restart, okg_krylov_stats* stats);
 
 /* ---- per-operator entry points on DEVICE pointers (parity + composition) ----
  * single-slab contexts only (OKG_EINVAL when nslabs > 1) */
@@ -287,6 +300,13 @@ enum okg_kernel_id {
   OKG_KT_COUNT = 8
 };
 int okg_kernel_timing(okg_ctx* ctx, int32_t which, int32_t reps, double* avg_ms, double* bytes);
+/* okg_kernel_timing with flags: OKG_KT_COLD = overwrite a 2 x L2-size scratch
+ * buffer before every launch and bracket each launch alone with events (the
+ * kernel reads its operands from HBM, as ncu's cold-cache replay does);
+ * OKG_KT_NO_PDL = launch without programmatic dependent launch */
+enum { OKG_KT_COLD = 1, OKG_KT_NO_PDL = 2 };
+int okg_kernel_timing_ex(okg_ctx* ctx, int32_t which, int32_t reps, int32_t flags, double* avg_ms,
+                         double* bytes);
 
 /* ---- device memory helpers (so a C/ctypes caller needs no CUDA headers) ---- */
 int okg_device_alloc(int32_t device, size_t bytes, void** ptr);

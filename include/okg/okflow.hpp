@@ -252,17 +252,34 @@ class SchurContext {
   // ctx.Me = assemble_coefficient_mass(mesh, u)   (model.hpp:184-185)
   void set_linearization(const Vector& u) {
     if (static_cast<long>(u.size()) != info_.num_vertices) throw std::invalid_argument("linearization: size mismatch");
-    check(okg_linearize_host(h_, u.data()));
+    check(okg_linearize_host_n(h_, u.data(), static_cast<int64_t>(u.size())));
     me_set_ = true;
   }
   void clear_linearization() {
     check(okg_clear_linearization(h_));
     me_set_ = false;
   }
-  Vector apply(int kind, const Vector& x, size_t out_size, int level = 0) const {
-    Vector y(out_size);
-    check(okg_apply_host(h_, kind, level, x.data(), y.data()));
+  // one operator (OKG_OP_*) on host vectors; the output length follows from the kind
+  // and level, a wrong input length is std::invalid_argument (operator.hpp:22-25)
+  Vector apply(int kind, const Vector& x, int level = 0) const {
+    Vector y(out_size(kind, level));
+    check(okg_apply_host_n(h_, kind, level, x.data(), static_cast<int64_t>(x.size()), y.data(),
+                           static_cast<int64_t>(y.size())));
     return y;
+  }
+  size_t out_size(int kind, int level = 0) const {
+    const int nl = info_.levels;
+    auto lvl = [&](int l) -> size_t {
+      if (l < 0 || l >= nl) throw std::invalid_argument("level out of range");
+      return static_cast<size_t>(info_.level_size[l]);
+    };
+    switch (kind) {
+      case OKG_OP_SHAT: case OKG_OP_VCYCLE: case OKG_OP_PROLONG: return lvl(level);
+      case OKG_OP_RESTRICT: return lvl(level + 1);
+      case OKG_OP_BLOCK: case OKG_OP_JACOBIAN: return 2 * static_cast<size_t>(info_.num_vertices);
+      case OKG_OP_COARSE_SOLVE: return lvl(nl - 1);
+      default: return static_cast<size_t>(info_.num_vertices);
+    }
   }
   int nslabs() const { return info_.nslabs; }
 
@@ -301,13 +318,13 @@ struct LinearOperator {
 inline Vector apply_block(const SchurContext& ctx, const Vector& r) {
   const int n = ctx.rows();
   if (static_cast<int>(r.size()) != 2 * n) throw std::invalid_argument("block preconditioner: stacked size mismatch");
-  return ctx.apply(OKG_OP_BLOCK, r, 2 * static_cast<size_t>(n));
+  return ctx.apply(OKG_OP_BLOCK, r);
 }
 
 inline LinearOperator jacobian_operator(const SchurContext& ctx) {
   const int n = ctx.rows();
   return {2 * n, 2 * n,
-          [&ctx, n](const Vector& x, Vector& y) { y = ctx.apply(OKG_OP_JACOBIAN, x, 2 * static_cast<size_t>(n)); },
+          [&ctx](const Vector& x, Vector& y) { y = ctx.apply(OKG_OP_JACOBIAN, x); },
           "coupled-jacobian"};
 }
 
@@ -317,14 +334,20 @@ inline LinearOperator block_preconditioner(const SchurContext& ctx) {
 }
 
 // gmres(jacobian_operator(ctx), block_preconditioner(ctx), b, ...)  (krylov.hpp:44-152),
-// run entirely on the device.
+// run entirely on the device.  Unlike the reference's gmres, which takes any pair of
+// LinearOperators (krylov.hpp:44-46), this one is specialised to the Newton path's
+// operator pair -- the coupled Jacobian right-preconditioned by the block-triangular
+// preconditioner -- because both live on the device as fused kernels; an arbitrary
+// host LinearOperator would need a host round trip per Arnoldi step.  Its arguments
+// and KrylovResult fields otherwise mean what the reference's do.
 inline KrylovResult gmres(const SchurContext& ctx, const Vector& b, double rel_tol, int max_iter, int restart = 0) {
   const int n = ctx.rows();
   if (static_cast<int>(b.size()) != 2 * n) throw std::invalid_argument("gmres: rhs dimension mismatch");
   okg_krylov_stats ks;
   KrylovResult r;
   r.x.resize(b.size());
-  check(okg_gmres_host(ctx.handle(), b.data(), r.x.data(), rel_tol, max_iter, restart, &ks));
+  check(okg_gmres_host_n(ctx.handle(), b.data(), r.x.data(), static_cast<int64_t>(b.size()), rel_tol, max_iter,
+                         restart, &ks));
   r.iterations = ks.iterations;
   r.converged = ks.converged != 0;
   r.stagnated = ks.stagnated != 0;
@@ -339,8 +362,8 @@ inline std::pair<Vector, Vector> residual(const State& next, const State& old, c
   if (next.u.size() != old.u.size() || next.w.size() != old.w.size() || next.u.size() != n)
     throw std::invalid_argument("residual: states do not match the mesh");
   Vector r1(n), r2(n);
-  check(okg_residual_host(ctx.handle(), next.u.data(), next.w.data(), old.u.data(), old.w.data(), r1.data(),
-                          r2.data()));
+  check(okg_residual_host_n(ctx.handle(), next.u.data(), next.w.data(), old.u.data(), old.w.data(),
+                            static_cast<int64_t>(n), r1.data(), r2.data()));
   return {r1, r2};
 }
 

@@ -386,13 +386,14 @@ class SchurContext:
     def apply(self, kind: int, x: np.ndarray, level: int = 0) -> np.ndarray:
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty(self._out_size(kind, level))
-        check(lib.okg_apply_host(self.handle, kind, level, x.ctypes.data_as(_lib._dp), y.ctypes.data_as(_lib._dp)))
+        check(lib.okg_apply_host_n(self.handle, kind, level, x.ctypes.data_as(_lib._dp), x.size,
+                                   y.ctypes.data_as(_lib._dp), y.size))
         return y
 
     def linearize(self, u: np.ndarray):
         """ctx.Me = assemble_coefficient_mass(mesh, u)  (model.hpp:184-185)."""
         u = np.ascontiguousarray(u, dtype=np.float64)
-        check(lib.okg_linearize_host(self.handle, u.ctypes.data_as(_lib._dp)))
+        check(lib.okg_linearize_host_n(self.handle, u.ctypes.data_as(_lib._dp), u.size))
         self.Me_set = True
 
     def linearize_dev(self, u: DeviceArray):
@@ -405,9 +406,11 @@ class SchurContext:
 
     def residual(self, nxt: State, old: State) -> Tuple[np.ndarray, np.ndarray]:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (nxt.u, nxt.w, old.u, old.w)]
+        if any(a.size != arrs[0].size for a in arrs):
+            raise InvalidArgument("residual: states do not match the mesh")
         r1 = np.empty(self.n)
         r2 = np.empty(self.n)
-        check(lib.okg_residual_host(self.handle, *[a.ctypes.data_as(_lib._dp) for a in arrs],
+        check(lib.okg_residual_host_n(self.handle, *[a.ctypes.data_as(_lib._dp) for a in arrs], arrs[0].size,
                                     r1.ctypes.data_as(_lib._dp), r2.ctypes.data_as(_lib._dp)))
         return r1, r2
 
@@ -415,7 +418,7 @@ class SchurContext:
         b = np.ascontiguousarray(b, dtype=np.float64)
         x = np.empty(2 * self.n)
         ks = _lib.KrylovStats()
-        check(lib.okg_gmres_host(self.handle, b.ctypes.data_as(_lib._dp), x.ctypes.data_as(_lib._dp), rel_tol,
+        check(lib.okg_gmres_host_n(self.handle, b.ctypes.data_as(_lib._dp), x.ctypes.data_as(_lib._dp), b.size, rel_tol,
                                  max_iter, restart, C.byref(ks)))
         nn = min(ks.n_residual_norms, 512)
         return KrylovResult(x, ks.iterations, list(ks.residual_norms[:nn]), bool(ks.converged),

@@ -29,6 +29,7 @@ OP_S_INV_APPROX, OP_BLOCK, OP_JACOBIAN, OP_NONLINEAR, OP_COARSE_SOLVE, OP_SSOR_M
 OKG_MAX_NEWTON = 64
 
 KT_NAMES = ["smooth", "resid", "pre2", "post_acc", "cheb", "jacobian", "restrict", "prolong"]
+KT_COLD, KT_NO_PDL = 1, 2
 
 
 class Params(C.Structure):
@@ -166,7 +167,13 @@ _SIGS = {
     "okg_apply_host": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
     "okg_residual_host": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp]),
     "okg_gmres_host": (C.c_int, [_vp, _dp, _dp, C.c_double, C.c_int32, C.c_int32, C.POINTER(KrylovStats)]),
+    "okg_apply_host_n": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.c_int64, _dp, C.c_int64]),
+    "okg_linearize_host_n": (C.c_int, [_vp, _dp, C.c_int64]),
+    "okg_residual_host_n": (C.c_int, [_vp, _dp, _dp, _dp, _dp, C.c_int64, _dp, _dp]),
+    "okg_gmres_host_n": (C.c_int, [_vp, _dp, _dp, C.c_int64, C.c_double, C.c_int32, C.c_int32,
+                                   C.POINTER(KrylovStats)]),
     "okg_kernel_timing": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp]),
+    "okg_kernel_timing_ex": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _dp, _dp]),
     "okg_device_alloc": (C.c_int, [C.c_int32, C.c_size_t, C.POINTER(_vp)]),
     "okg_device_free": (C.c_int, [_vp]),
     "okg_memcpy_h2d": (C.c_int, [_vp, _vp, C.c_size_t]),

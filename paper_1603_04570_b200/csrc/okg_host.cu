@@ -3157,6 +3157,39 @@ int okg_gmres_host(okg_ctx* c, const double* b, double* x, double rel_tol, int32
   return st;
 }
 
+// ---- length-checked host-pointer entry points: the caller passes its array lengths and a
+// mismatch is std::invalid_argument, as the reference's LinearOperator::apply
+// (operator.hpp:22-25), gmres (krylov.hpp:48-51) and residual (model.hpp:126-127) throw
+int okg_apply_host_n(okg_ctx* c, int32_t kind, int32_t level, const double* x, int64_t nx, double* y, int64_t ny) {
+  if (!c || !x || !y) return fail(OKG_EINVAL, "okg_apply_host_n: null argument");
+  size_t nin = 0, nout = 0;
+  const int st = guard(c, [&] { apply_sizes(slab0(c), kind, level, nin, nout); });
+  if (st != OKG_OK) return st;
+  if (nx != (int64_t)nin) return fail(OKG_EINVAL, "operator %d: input dimension mismatch (%lld, expected %zu)", kind, (long long)nx, nin);
+  if (ny != (int64_t)nout) return fail(OKG_EINVAL, "operator %d: output dimension mismatch (%lld, expected %zu)", kind, (long long)ny, nout);
+  return okg_apply_host(c, kind, level, x, y);
+}
+
+int okg_linearize_host_n(okg_ctx* c, const double* u, int64_t n) {
+  if (!c || !u) return fail(OKG_EINVAL, "okg_linearize_host_n: null argument");
+  if (n != (int64_t)slab0(c)->N) return fail(OKG_EINVAL, "assemble_coefficient_mass: vector length mismatch");
+  return okg_linearize_host(c, u);
+}
+
+int okg_residual_host_n(okg_ctx* c, const double* un, const double* wn, const double* uo, const double* wo, int64_t n,
+                        double* r1, double* r2) {
+  if (!c) return fail(OKG_EINVAL, "okg_residual_host_n: null argument");
+  if (n != (int64_t)slab0(c)->N) return fail(OKG_EINVAL, "residual: states do not match the mesh");
+  return okg_residual_host(c, un, wn, uo, wo, r1, r2);
+}
+
+int okg_gmres_host_n(okg_ctx* c, const double* b, double* x, int64_t n, double rel_tol, int32_t max_iter,
+                     int32_t restart, okg_krylov_stats* stats) {
+  if (!c) return fail(OKG_EINVAL, "okg_gmres_host_n: null argument");
+  if (n != 2 * (int64_t)slab0(c)->N) return fail(OKG_EINVAL, "gmres: rhs dimension mismatch");
+  return okg_gmres_host(c, b, x, rel_tol, max_iter, restart, stats);
+}
+
 // ---- device-pointer entry points (one slab) ------------------------------------------------
 int okg_linearize(okg_ctx* c, const double* u_dev) {
   if (!c || !u_dev) return fail(OKG_EINVAL, "okg_linearize: null argument");
@@ -3229,7 +3262,7 @@ int okg_slab_stream(okg_ctx* c, int32_t slab, void** stream) {
 }  // extern "C"
 
 template <int DIM>
-static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, double* bytes) {
+static void kernel_timing_impl(okg_ctx* c, int which, int reps, int flags, double* avg_ms, double* bytes) {
   Level& L0 = c->lv[0];
   const Grid& g = L0.g;
   const double om = c->p.mg_omega;
@@ -3306,19 +3339,46 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, double* avg_ms, 
     case OKG_KT_PROLONG: *bytes = (L0.tiled ? 3 * N + Nc : 2 * N + Nc) * B; break;
   }
   bool had_lin = c->have_lin;
+  const bool saved_pdl = c->p.disable_pdl;
+  if (flags & OKG_KT_NO_PDL) c->p.disable_pdl = 1;
   for (int i = 0; i < 3; ++i) run_once();
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, c->stream));
-  for (int i = 0; i < reps; ++i) run_once();
-  CK(cudaEventRecord(e1, c->stream));
-  CK(cudaEventSynchronize(e1));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, e0, e1));
+  double total_ms = 0.0;
+  if (flags & OKG_KT_COLD) {
+    // L2-cold: before every launch, overwrite a scratch buffer of twice the L2 size
+    // (126 MB on B200), then bracket the launch alone with events
+    int dev = 0, l2 = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const size_t fl = 2 * (size_t)std::max(l2, 64 << 20);
+    void* scratch = nullptr;
+    CK(cudaMalloc(&scratch, fl));
+    for (int i = 0; i < reps; ++i) {
+      CK(cudaMemsetAsync(scratch, i & 0xff, fl, c->stream));
+      CK(cudaEventRecord(e0, c->stream));
+      run_once();
+      CK(cudaEventRecord(e1, c->stream));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      total_ms += ms;
+    }
+    cudaFree(scratch);
+  } else {
+    CK(cudaEventRecord(e0, c->stream));
+    for (int i = 0; i < reps; ++i) run_once();
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    total_ms = ms;
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  *avg_ms = (double)ms / reps;
+  c->p.disable_pdl = saved_pdl;
+  *avg_ms = total_ms / reps;
   c->have_lin = had_lin;
 }
 
@@ -3327,7 +3387,13 @@ extern "C" {
 int okg_kernel_timing(okg_ctx* c, int32_t which, int32_t reps, double* avg_ms, double* bytes) {
   if (!c || !avg_ms || !bytes || reps < 1) return fail(OKG_EINVAL, "okg_kernel_timing: bad argument");
   if (c->handle) return fail(OKG_EINVAL, "okg_kernel_timing: time one slab (okg_create_rank) instead");
-  return guard(c, [&] { DISPATCH(c, kernel_timing_impl, c, which, reps, avg_ms, bytes); });
+  return guard(c, [&] { DISPATCH(c, kernel_timing_impl, c, which, reps, 0, avg_ms, bytes); });
+}
+
+int okg_kernel_timing_ex(okg_ctx* c, int32_t which, int32_t reps, int32_t flags, double* avg_ms, double* bytes) {
+  if (!c || !avg_ms || !bytes || reps < 1) return fail(OKG_EINVAL, "okg_kernel_timing_ex: bad argument");
+  if (c->handle) return fail(OKG_EINVAL, "okg_kernel_timing_ex: time one slab (okg_create_rank) instead");
+  return guard(c, [&] { DISPATCH(c, kernel_timing_impl, c, which, reps, (int)flags, avg_ms, bytes); });
 }
 
 int okg_device_alloc(int32_t device, size_t bytes, void** ptr) {
