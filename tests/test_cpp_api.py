@@ -28,3 +28,19 @@ def test_cpp_api_on_gpu():
     out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "all C++ host-API checks passed" in out.stdout
+
+
+ADAPTER = os.path.join(ROOT, "tests", "cpp", "test_okflow_adapter")
+
+
+@pytest.mark.gpu
+def test_okflow_adapter_time_loop_on_gpu():
+    """include/okg/okflow_adapter.hpp: the reference's own time loop (okflow types) with
+    make_schur_context / newton_solve swapped to okg:: matches the reference step by step
+    (binary built by __graft_entry__.build() against the reference headers)."""
+    if not os.path.exists(ADAPTER):
+        pytest.skip("adapter check not built (needs the reference headers at build time)")
+    out = subprocess.run([ADAPTER], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "all okflow-adapter checks passed" in out.stdout
+    print(out.stdout)
