@@ -79,9 +79,6 @@ typedef struct okg_params {
                                device `device + r` (peer copies over NVLink) */
   int32_t tail_cluster;     /* CTAs in the tail's cluster (they split the rows of the dense
                                coarse inverse): 0 = default (enough for <= 96 KB each), 1..16 */
-  int32_t cheb_fuse;        /* Chebyshev steps two per pass (2D, one slab; bit-identical):
-                               > 0 = on with this many rows per tile (4 measured best),
-                               <= 0 = one step per pass (default) */
   int32_t cheby_ssor;       /* SolverConfig::cheby_precond: 0 = "jacobi", 1 = "ssor" (SSOR
                                sweeps as hyperplane wavefronts, one slab only) */
   int32_t coarse_split;     /* coarsest level above 2000 unknowns (device-factorised inverse):
@@ -95,11 +92,6 @@ typedef struct okg_params {
                                the latency-bound bottom of each V-cycle is one HBM-streaming
                                matvec; 0 = default (3D 1000, 2D 1100: the cluster tail's levels),
                                < 0 = never */
-  int32_t mg_cluster;       /* V(2,2), one slab, collapsed bottom: from the first level with at most
-                               this many vertices down to the collapsed bottom, the V-cycle runs as
-                               ONE 16-CTA thread-block-cluster kernel with the levels in distributed
-                               shared memory (okg_cluster.cuh); bit-identical, but measured slower
-                               than the chained level kernels, so opt-in: <= 0 = never (default) */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -145,7 +137,6 @@ typedef struct okg_info {
   int32_t tail_cluster;       /* CTAs in the tail's thread-block cluster */
   int32_t coarse_rows;        /* rows of the coarse inverse this slab multiplies */
   int32_t collapse_level;     /* first level applied as one dense operator (-1: none) */
-  int32_t mc_start;           /* first level of the cluster V-cycle (-1: none) */
 } okg_info;
 
 /* operator kinds for okg_apply (same numbering as the oracle's) */

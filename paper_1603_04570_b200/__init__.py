@@ -77,8 +77,8 @@ class SolverConfig:
     def to_params(self, device: int = 0, shat_perturb: float = 0.0, use_graphs: bool = True,
                   tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
                   mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
-                  tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0,
-                  mg_collapse: int = 0, mg_cluster: int = 0) -> _lib.Params:
+                  tail_cluster: int = 0, coarse_split: int = 0,
+                  mg_collapse: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -95,10 +95,8 @@ class SolverConfig:
         p.nslabs = nslabs
         p.slab_devices = 1 if slab_devices else 0
         p.tail_cluster = tail_cluster
-        p.cheb_fuse = cheb_fuse
         p.coarse_split = coarse_split
         p.mg_collapse = mg_collapse
-        p.mg_cluster = mg_cluster
         p.cheby_ssor = 1 if self.cheby_precond == "ssor" else 0
         return p
 
@@ -307,8 +305,7 @@ class SchurContext:
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
                  pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
                  rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None,
-                 tail_cluster: int = 0, cheb_fuse: int = 0, coarse_split: int = 0, mg_collapse: int = 0,
-                 mg_cluster: int = 0):
+                 tail_cluster: int = 0, coarse_split: int = 0, mg_collapse: int = 0):
         """nslabs > 1: x-plane slab decomposition, one host thread + stream per
         slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
         `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
@@ -318,8 +315,7 @@ class SchurContext:
         self.device = device
         self.handle = C.c_void_p()
         params = cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl, mg_fuse,
-                               nslabs, slab_devices, tail_cluster, cheb_fuse, coarse_split,
-                               mg_collapse, mg_cluster)
+                               nslabs, slab_devices, tail_cluster, coarse_split, mg_collapse)
         if rank is None:
             check(lib.okg_create(C.byref(params), C.byref(self.handle)))
         else:
@@ -348,7 +344,6 @@ class SchurContext:
         self.tiled_levels = [l for l in range(self.levels) if (info.tiled_mask >> l) & 1]
         self.coarse_rows = int(info.coarse_rows)
         self.collapse_level = int(info.collapse_level)
-        self.mc_start = int(info.mc_start)
         self.nslabs = int(info.nslabs)
         self.rep_level = int(info.rep_level)
         self.slab_planes = [(int(info.slab_ilo[r]), int(info.slab_ihi[r])) for r in range(self.nslabs)]

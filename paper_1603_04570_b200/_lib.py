@@ -46,11 +46,10 @@ class Params(C.Structure):
         ("device", C.c_int32), ("use_graphs", C.c_int32), ("tiled_min_n", C.c_int32),
         ("tail_max_vertices", C.c_int32), ("disable_pdl", C.c_int32),
         ("mg_fuse", C.c_int32), ("nslabs", C.c_int32), ("slab_devices", C.c_int32),
-        ("tail_cluster", C.c_int32), ("cheb_fuse", C.c_int32),
+        ("tail_cluster", C.c_int32),
         ("cheby_ssor", C.c_int32),
         ("coarse_split", C.c_int32),
         ("mg_collapse", C.c_int32),
-        ("mg_cluster", C.c_int32),
     ]
 
 
@@ -82,7 +81,6 @@ class Info(C.Structure):
         ("nslabs", C.c_int32), ("rep_level", C.c_int32),
         ("slab_ilo", C.c_int32 * 16), ("slab_ihi", C.c_int32 * 16), ("tail_cluster", C.c_int32),
         ("coarse_rows", C.c_int32), ("collapse_level", C.c_int32),
-        ("mc_start", C.c_int32),
     ]
 
 

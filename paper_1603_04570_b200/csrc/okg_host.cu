@@ -35,7 +35,6 @@
 #include "../../include/okg.h"
 #include "okg_kernels.cuh"
 #include "okg_diag.cuh"
-#include "okg_cheb2.cuh"
 #include "okg_ssor.cuh"
 #include "okg_nccl.h"
 #include "okg_cusolver.h"
@@ -101,6 +100,7 @@ struct Level {
   HostOp shat;
   bool tiled = false;
   bool fused = false;  // V(2,2) through k_mg_down / k_mg_up (okg_vcycle.cuh)
+  bool rr = false;     // tiled level, one slab: residual + restriction in one launch (okg_rr.cuh)
   Tiling tl{};
   unsigned tl_blocks = 0;
   Tiling tlc{};  // the C-block kernels' tiling (okg_tiled_c.cuh): same tiles, their own x-chunks
@@ -135,20 +135,13 @@ struct okg_ctx {
   size_t coarse_ld = 0;
   int coarse_nb = 0;  // > 0: one slab, symmetric packed blocks (k_coarse_sym)
   double *coarse_R = nullptr, *coarse_C = nullptr;
-  unsigned* coarse_cnt = nullptr;  // row-block counters of k_coarse_sym1
   // collapsed bottom of the V-cycle (okg_params.mg_collapse): level collapse_level and
   // everything below it as one symmetric dense operator, packed like the coarse inverse
   int collapse_level = -1, col_nb = 0;
   double *col_A = nullptr, *col_R = nullptr, *col_C = nullptr;
-  unsigned* col_cnt = nullptr;
-  bool coarse1 = false;  // coarse_sym_apply: one launch (env OKG_COARSE1=1) or two
   int tail_start = -1;  // first level run by the cluster tail kernel (-1: none)
   int tail_cluster = 1;  // CTAs in the tail's thread-block cluster
   double* tail_tab = nullptr;  // tail weight tables (okg_tail.cuh)
-  // cluster V-cycle (okg_cluster.cuh): levels mc_start .. collapse_level-1 and the
-  // collapsed bottom in one 16-CTA cluster launch (-1: none)
-  int mc_start = -1;
-  double* mc_tab = nullptr;
   double b_int = 0;
   double* b_tab = nullptr;
   Nonlin nl;
@@ -161,7 +154,7 @@ struct okg_ctx {
   double *gb = nullptr, *gx = nullptr, *gr = nullptr, *pin = nullptr, *pz = nullptr, *pw = nullptr,
          *gt = nullptr;
   // preconditioner scratch
-  double* cr2 = nullptr;  // second Chebyshev residual buffer (two-step kernel, okg_cheb2.cuh)
+  double* cr2 = nullptr;  // scratch of the SSOR-preconditioned Chebyshev
   double* cad = nullptr;  // A d of the SSOR-preconditioned Chebyshev
   bool ssor = false;      // cheby_precond == "ssor" (okg_ssor.cuh)
   int ssor_cluster = 1;   // CTAs of the sweep kernels' cluster
@@ -686,19 +679,13 @@ static void copy(okg_ctx* c, const double* x, double* y, size_t n) {
   CK(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
 }
 
-// y = A x, A symmetric as packed CB-blocks (coarsest inverse / collapsed bottom):
-// two launches (k_coarse_sym, k_coarse_sym_sum), or with OKG_COARSE1=1 in the
-// environment at okg_create one (k_coarse_sym1: the last contributor of a row block
-// sums it) -- same bits, but measured slower (the row sums pile up at the tail of
-// the grid): 128^3 45.0 vs 44.4 ms, 400^3 976 vs 957 ms, 2D 2048^2 56.7 vs 56.5 ms
+// y = A x, A symmetric as packed CB-blocks (coarsest inverse / collapsed bottom): every
+// block is streamed once and forms both of its products (k_coarse_sym), then the
+// partials of a row are summed in a fixed order (k_coarse_sym_sum).  (One launch with a
+// last-contributor row sum was bit-identical but slower -- DESIGN section 5 item 10.)
 static void coarse_sym_apply(okg_ctx* c, int n, int nb, const double* A, const double* x, double* R, double* C,
-                             double* y, unsigned* cnt) {
+                             double* y) {
   const unsigned nblk = (unsigned)(nb * (nb + 1) / 2);
-  if (c->coarse1) {
-    launch(c, k_coarse_sym1, nblk, 256, 0, n, nb, A, x, R, C, y, cnt);
-    note(c);
-    return;
-  }
   launch(c, k_coarse_sym, nblk, 256, 0, n, A, x, R, C);
   note(c);
   launch(c, k_coarse_sym_sum, (unsigned)nb, CB * CSEG, 0, n, nb, (const double*)R, (const double*)C, y);
@@ -725,7 +712,7 @@ static void coarse_solve(okg_ctx* c, const double* b, double* y) {
   }
   if (c->coarse_nb > 0) {  // one slab: half the bytes through the symmetric block triangle
     const int nb = c->coarse_nb;
-    coarse_sym_apply(c, c->nc, nb, c->Ainv, b, c->coarse_R, c->coarse_C, y, c->coarse_cnt);
+    coarse_sym_apply(c, c->nc, nb, c->Ainv, b, c->coarse_R, c->coarse_C, y);
     return;
   }
   double* tgt = c->coarse_split ? L.ea : y;
@@ -766,7 +753,6 @@ static void collapse_levels(okg_ctx* c, int lc) {
     c->col_A = dalloc(c, nblk * CB * CB);
     c->col_R = dalloc(c, nblk * CB);
     c->col_C = dalloc(c, nblk * CB);
-    c->col_cnt = reinterpret_cast<unsigned*>(dalloc(c, nb));  // zeroed
     k_coarse_pack<<<148 * 8, 256, 0, c->stream>>>(N, nb, F, c->col_A);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
@@ -832,7 +818,6 @@ static void coarse_inverse_device(okg_ctx* c, const std::vector<double>& Ad, int
       c->Ainv = dalloc(c, nblk * CB * CB);
       c->coarse_R = dalloc(c, nblk * CB);
       c->coarse_C = dalloc(c, nblk * CB);
-      c->coarse_cnt = reinterpret_cast<unsigned*>(dalloc(c, nb));  // zeroed
       k_coarse_pack<<<148 * 8, 256, 0, c->stream>>>(nc, nb, F, c->Ainv);
       c->coarse_nb = nb;
     } else {
@@ -902,42 +887,6 @@ static void run_tail(okg_ctx* c, int l0, const double* rhs, double* out) {
   note(c);
 }
 
-// levels mc_start .. collapse_level-1 + the collapsed bottom in one cluster launch
-// (okg_cluster.cuh); instantiated for power-of-two levels ending at the default
-// collapse level (3D 9^3, 2D 33^2)
-template <int DIM, class F>
-static bool mc_dispatch(int n0, int nl, F&& f) {
-  using I = std::integral_constant<int, 1>;
-  using II = std::integral_constant<int, 2>;
-  if constexpr (DIM == 3) {
-    if (n0 == 32 && nl == 2) f(std::integral_constant<int, 32>{}, II{});
-    else if (n0 == 16 && nl == 1) f(std::integral_constant<int, 16>{}, I{});
-    else return false;
-  } else {
-    if (n0 == 256 && nl == 3) f(std::integral_constant<int, 256>{}, std::integral_constant<int, 3>{});
-    else if (n0 == 128 && nl == 2) f(std::integral_constant<int, 128>{}, II{});
-    else if (n0 == 64 && nl == 1) f(std::integral_constant<int, 64>{}, I{});
-    else return false;
-  }
-  return true;
-}
-
-template <int DIM>
-static void run_mc(okg_ctx* c, int l0, const double* rhs, double* out) {
-  MCArgs<DIM> A;
-  std::memset(&A, 0, sizeof A);
-  A.tabs = c->mc_tab;
-  A.omega = c->p.mg_omega;
-  A.rhs = rhs;
-  A.out = out;
-  A.colA = c->col_A;
-  mc_dispatch<DIM>(c->lv[l0].g.n, c->collapse_level - l0, [&](auto N0, auto NL) {
-    constexpr int n0 = decltype(N0)::value, nl = decltype(NL)::value;
-    launch_cluster(c, k_mg_cluster<DIM, n0, nl>, (unsigned)MC_C, MC_NT, mc_smem_bytes<DIM, n0, nl>(), A);
-  });
-  note(c);
-}
-
 template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc);
 
@@ -969,13 +918,9 @@ template <int DIM>
 static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc) {
   Level& L = c->lv[l];
   const int last = static_cast<int>(c->lv.size()) - 1;
-  if (l == c->mc_start && !acc) {
-    run_mc<DIM>(c, l, rhs, out);
-    return;
-  }
   if (l == c->collapse_level && !acc) {  // the whole cycle below l in one matvec
     const int nb = c->col_nb;
-    coarse_sym_apply(c, (int)L.g.N, nb, c->col_A, rhs, c->col_R, c->col_C, out, c->col_cnt);
+    coarse_sym_apply(c, (int)L.g.N, nb, c->col_A, rhs, c->col_R, c->col_C, out);
     return;
   }
   if (l == c->tail_start && !acc && l > 0) {
@@ -1022,10 +967,22 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
     note(c);
   }
   // ---- residual, restriction, coarse correction (multigrid.hpp:106-110)
+  Level& C = c->lv[l + 1];
+  if (L.tiled && L.rr) {
+    // residual + restriction in one launch (okg_rr.cuh): r never goes to memory
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_resid_restrict<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)RRGeom<DIM>::SMEM));
+      attr = true;
+    }
+    launch(c, k_resid_restrict<DIM>, rr_grid<DIM>(C.g), RRGeom<DIM>::NT, RRGeom<DIM>::SMEM, L.g, C.g, op,
+           (const double*)cur, rhs, C.b);
+    note(c);
+  } else {
   exchange(c, l, cur);
   if (L.tiled) tiled<DIM, L_PLAIN, T_RESID>(c, L, L.shat, targs(cur, rhs, L.res, nullptr, 0.0));
   else op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
-  Level& C = c->lv[l + 1];
   exchange(c, l, L.res);
   {
     // coarse vertices G with 2G in this slab's planes (all of them when not split)
@@ -1034,6 +991,7 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
     launch(c, k_restrict<DIM>, own(gcr), BS, 0, L.g, gcr, (const double*)L.res, C.b);
     note(c);
     if (C.rep && !L.rep) allgather_planes(c, l + 1, C.b);
+  }
   }
   mg_level<DIM>(c, l + 1, C.b, C.x, false);
   // ---- prolongation + post-smoothing (multigrid.hpp:111-115)
@@ -1096,38 +1054,6 @@ static void shat_inv(okg_ctx* c, const double* b, double* x, int cycles) {
 template <int DIM>
 static void cheb_ssor(okg_ctx* c, const HostOp& A, const double* b, double* x);
 
-// two Chebyshev steps in one pass (2D only; okg_cheb2.cuh)
-template <int DIM>
-static void cheb2_launch(okg_ctx* c, const Op<DIM>& o, const Cheb2Args& a) {
-  if constexpr (DIM == 2) {
-    const Level& L = c->lv[0];
-    auto run = [&](auto TIc) {
-      constexpr int TI = decltype(TIc)::value;
-      static bool attr = false;
-      if (!attr) {
-        CK(cudaFuncSetAttribute(k_cheb2<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cheb2_smem_bytes<TI>()));
-        attr = true;
-      }
-      // the level's tiling re-cut into TI-row chunks (same boundary list)
-      Tiling t = L.tl;
-      const int nci = std::max(0, t.ci1 - t.ci0);
-      t.ichunk = TI;
-      t.ncore = t.ktiles * ((nci + TI - 1) / TI);
-      const unsigned blocks = (unsigned)t.ncore + (t.nbnd + TileCfg<2>::NT - 1) / TileCfg<2>::NT;
-      launch(c, k_cheb2<TI>, blocks, TileCfg<2>::NT, cheb2_smem_bytes<TI>(), L.g, o, t, a);
-      note(c);
-    };
-    const int ti = c->p.cheb_fuse > 0 ? c->p.cheb_fuse : 4;  // rows per tile (measured best: see DESIGN)
-    if (ti >= 8) run(std::integral_constant<int, 8>{});
-    else if (ti >= 4) run(std::integral_constant<int, 4>{});
-    else run(std::integral_constant<int, 2>{});
-  } else {
-    (void)c;
-    (void)o;
-    (void)a;
-  }
-}
-
 // ---- Chebyshev (krylov.hpp:158-202) ---------------------------------------------
 template <int DIM>
 static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
@@ -1146,43 +1072,12 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
     copy(c, dcur + g.lo, x + g.lo, g.hi - g.lo);
     return;
   }
-  // 2D, one slab, tiled finest level: two steps per pass (okg_cheb2.cuh)
-  // (opt-in since the PDL trigger change: one step per pass measured 0.4 % faster per
-  // 2D 2048^2 step, 62.4 vs 62.7 ms)
-  const bool two = DIM == 2 && c->lv[0].tiled && c->nslabs == 1 && c->p.cheb_fuse > 0;
-  double* rcur = nullptr;  // r_j (b before the first step)
+  // (two steps per pass -- a halo-2 tile -- was bit-identical but 0.4 % slower per 2D step
+  // and is gone: DESIGN section 5)
   for (int j = 0; j + 1 < k; ++j) {
     const int last = (j == k - 2);
-    if (two && j + 2 < k) {
-      Cheb2Args a2;
-      a2.d = dcur;
-      a2.r = j == 0 ? b : rcur;
-      a2.x = j == 0 ? dcur : x;
-      a2.d_out = dnxt;
-      a2.r_out = (rcur == c->cr) ? c->cr2 : c->cr;
-      a2.x_out = x;
-      a2.c1a = c->cheb_c1[j];
-      a2.c2a = c->cheb_c2[j];
-      a2.c1b = c->cheb_c1[j + 1];
-      a2.c2b = c->cheb_c2[j + 1];
-      a2.last = (j + 1 == k - 2);
-      cheb2_launch<DIM>(c, o, a2);
-      rcur = a2.r_out;
-      std::swap(dcur, dnxt);
-      ++j;  // two steps done
-      continue;
-    }
     exchange(c, 0, dcur);
-    if (two) {  // a single step left over (odd count): reads rcur, writes the other buffer
-      TArgs a = targs(dcur, j == 0 ? b : rcur, (rcur == c->cr) ? c->cr2 : c->cr, x, 0.0);
-      a.x2 = j == 0 ? dcur : x;
-      a.y2 = dnxt;
-      a.c1 = c->cheb_c1[j];
-      a.c2 = c->cheb_c2[j];
-      a.last = last;
-      tiled<DIM, L_PLAIN, T_CHEB>(c, c->lv[0], A, a);
-      rcur = (rcur == c->cr) ? c->cr2 : c->cr;
-    } else if (c->lv[0].tiled) {
+    if (c->lv[0].tiled) {
       TArgs a = targs(dcur, j == 0 ? b : c->cr, c->cr, x, 0.0);
       a.x2 = j == 0 ? dcur : x;
       a.y2 = dnxt;
@@ -1917,7 +1812,6 @@ template <int DIM>
 static void build(okg_ctx* c) {
   const okg_params& p = c->p;
   const UnitTables ut = build_unit_tables(DIM);
-  if (const char* e = std::getenv("OKG_COARSE1")) c->coarse1 = std::atoi(e) != 0;
   const int n = p.n;
   c->h = 1.0 / n;
   const double hd = ipow(c->h, DIM), hk = ipow(c->h, DIM - 2);
@@ -2072,6 +1966,14 @@ static void build(okg_ctx* c) {
     if (tmin > 0)
       for (Level& L : c->lv)
         if (L.g.n >= std::max(tmin, 2)) make_tiling<DIM>(c, L);
+    // fused residual + restriction on tiled levels that are not split across slabs
+    // (environment OKG_RR=0 at okg_create: the two separate kernels, for A/B runs)
+    {
+      const char* e = std::getenv("OKG_RR");
+      const bool want = !(e && std::atoi(e) == 0);
+      for (size_t l = 0; l + 1 < c->lv.size(); ++l)
+        c->lv[l].rr = want && c->lv[l].tiled && S == 1 && (c->lv[l].g.n % 2 == 0);
+    }
     // coarsest: dense SPD inverse (replaces CholeskyFactor, multigrid.hpp:82-83)
     Level& Lc = c->lv.back();
     const int nc = (int)Lc.g.N;
@@ -2186,63 +2088,6 @@ static void build(okg_ctx* c) {
         break;
       }
     if (lc > 0 && (c->nslabs == 1 || lc >= c->L_rep)) collapse_levels<DIM>(c, lc);
-  }
-  // cluster V-cycle above the collapsed bottom (okg_params.mg_cluster, okg_cluster.cuh)
-  // (opt-in: measured slower than the PDL-chained level kernels)
-  if (p.mg_cluster > 0 && c->collapse_level > 1 && c->nslabs == 1 && p.mg_pre == 2 && p.mg_post == 2) {
-    const int64_t vmax = p.mg_cluster;
-    for (int l = 1; l < c->collapse_level; ++l) {
-      if ((int64_t)c->lv[l].g.N > vmax) continue;
-      bool ok = false;
-      mc_dispatch<DIM>(c->lv[l].g.n, c->collapse_level - l, [&](auto N0, auto NL) {
-        constexpr int n0 = decltype(N0)::value, nl = decltype(NL)::value;
-        auto k = k_mg_cluster<DIM, n0, nl>;
-        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mc_smem_bytes<DIM, n0, nl>()) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-          cudaGetLastError();
-          return;
-        }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(MC_C);
-        cfg.blockDim = dim3(MC_NT);
-        cfg.dynamicSmemBytes = mc_smem_bytes<DIM, n0, nl>();
-        cudaLaunchAttribute at;
-        at.id = cudaLaunchAttributeClusterDimension;
-        at.val.clusterDim.x = MC_C;
-        at.val.clusterDim.y = 1;
-        at.val.clusterDim.z = 1;
-        cfg.attrs = &at;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, k, &cfg) != cudaSuccess) cudaGetLastError();
-        ok = ncl > 0;
-      });
-      if (!ok) break;
-      // tables: the cluster levels' class rows, then the restriction weights (as the tail)
-      const int NO = Traits<DIM>::NOFF, NCL = Traits<DIM>::NCLS;
-      const int nl = c->collapse_level - l;
-      std::vector<double> tt((size_t)mc_table_doubles<DIM>(nl), 0.0);
-      for (int q = 0; q < nl; ++q) {
-        const std::vector<double>& h = c->lv[l + q].shat.htab;
-        std::copy(h.begin(), h.end(), tt.begin() + (size_t)q * NCL * (NO + 1));
-      }
-      for (int cl = 0; cl < NCL; ++cl)
-        for (int o = 0; o < NO; ++o) {
-          bool in = true;
-          int cc = cl;
-          for (int d = DIM - 1; d >= 0; --d) {
-            const int cd = cc % 3, od = off_comp(DIM, o, d);
-            cc /= 3;
-            in = in && !(cd == 0 && od < 0) && !(cd == 2 && od > 0);
-          }
-          tt[(size_t)nl * NCL * (NO + 1) + cl * NO + o] = in ? (o == NO / 2 ? 1.0 : 0.5) : 0.0;
-        }
-      c->mc_tab = dalloc(c, tt.size());
-      CK(cudaMemcpyAsync(c->mc_tab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-      c->mc_start = l;
-      break;
-    }
   }
   if (p.use_graphs) capture_graphs<DIM>(c);
   CK(cudaStreamSynchronize(c->stream));
@@ -2846,7 +2691,6 @@ int okg_get_info(okg_ctx* h, okg_info* info) {
   info->tail_cluster = c->tail_start > 0 ? c->tail_cluster : 0;
   info->coarse_rows = c->coarse_big ? c->coarse_r1 - c->coarse_r0 : c->nc;
   info->collapse_level = c->collapse_level;
-  info->mc_start = c->mc_start;
   for (size_t l = 0; l < c->lv.size() && l < 31; ++l)
     if (c->lv[l].tiled) info->tiled_mask |= (1 << l);
   info->nslabs = h->handle ? h->nslabs : c->nslabs;

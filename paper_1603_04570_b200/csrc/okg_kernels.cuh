@@ -389,16 +389,13 @@ __global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __rest
 // loads issued 4 at a time), the segment sums then added in segment order: a fixed
 // order, so the result is deterministic.
 constexpr int CSEG = 4;
-// rows of block I (blockDim = CB * CSEG); COHERENT: the partials were written by other
-// CTAs of the running grid (k_coarse_sym1), so they are read through L2, not the
-// non-coherent path
-template <bool COHERENT>
+// rows of block I (blockDim = CB * CSEG)
 __device__ __forceinline__ void coarse_sym_rows(int nc, int nb, const double* __restrict__ R,
                                                 const double* __restrict__ Cp, double* __restrict__ y, int I) {
   __shared__ double part[CSEG][CB];
   const int t = threadIdx.x % CB, sg = threadIdx.x / CB;
   const size_t base = (size_t)I * (I + 1) / 2;
-  auto ld = [](const double* p) -> double { return COHERENT ? __ldcg(p) : __ldg(p); };
+  auto ld = [](const double* p) -> double { return __ldg(p); };
   // term q (0..nb-1): q <= I -> R(I, q), else C(q, I)
   auto term = [&](int q) -> double {
     return q <= I ? ld(R + (base + q) * CB + t) : ld(Cp + ((size_t)q * (q + 1) / 2 + I) * CB + t);
@@ -427,39 +424,7 @@ __device__ __forceinline__ void coarse_sym_rows(int nc, int nb, const double* __
 __global__ void __launch_bounds__(CB * CSEG) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
                                                               const double* __restrict__ Cp, double* __restrict__ y) {
   PDL_ENTRY();
-  coarse_sym_rows<false>(nc, nb, R, Cp, y, blockIdx.x);
-}
-
-// k_coarse_sym + k_coarse_sym_sum in one launch: every CTA counts its block into the
-// row blocks it feeds (I and, off the diagonal, J); the CTA that completes a row
-// block (nb contributions) sums it, in k_coarse_sym_sum's order (bit-identical), and
-// re-arms the counter for the next call.  cnt: nb zeroed counters.
-static_assert(CB * CSEG == 256, "k_coarse_sym1 runs both halves with one block shape");
-__global__ void __launch_bounds__(256) k_coarse_sym1(int nc, int nb, const double* __restrict__ Ap,
-                                                     const double* __restrict__ x, double* __restrict__ R,
-                                                     double* __restrict__ Cp, double* __restrict__ y,
-                                                     unsigned* __restrict__ cnt) {
-  PDL_ENTRY();
-  __shared__ int fin[2];
-  int I, J;
-  tri_index(blockIdx.x, I, J);
-  coarse_sym_block(nc, Ap, x, R, Cp, I, J);
-  __threadfence();  // this CTA's partials are visible before it is counted
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fin[0] = atomicAdd(cnt + I, 1u) == (unsigned)nb - 1 ? I : -1;
-    fin[1] = (I != J && atomicAdd(cnt + J, 1u) == (unsigned)nb - 1) ? J : -1;
-    __threadfence();
-  }
-  __syncthreads();
-#pragma unroll
-  for (int f = 0; f < 2; ++f) {
-    const int rb = fin[f];
-    if (rb < 0) continue;  // (CTA-uniform)
-    coarse_sym_rows<true>(nc, nb, R, Cp, y, rb);
-    if (threadIdx.x == 0) cnt[rb] = 0u;
-    __syncthreads();  // part[] reuse
-  }
+  coarse_sym_rows(nc, nb, R, Cp, y, blockIdx.x);
 }
 
 // setup: v = e_i (unit vector of length n)
@@ -964,6 +929,6 @@ __global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ 
 }  // namespace okg
 
 #include "okg_tiled_c.cuh"
+#include "okg_rr.cuh"
 #include "okg_vcycle.cuh"
 #include "okg_tail.cuh"  // uses slot_ok / op_row above
-#include "okg_cluster.cuh"

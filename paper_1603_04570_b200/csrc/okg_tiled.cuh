@@ -4,11 +4,14 @@
 // Why: the naive one-thread-per-vertex gather issues 15 (3D) global loads per
 // vertex; the L1/L2 traffic is ~7x the DRAM traffic and boundary vertices
 // make whole warps diverge.  Here a CTA owns a (TJ x TK) tile of the (y,z)
-// plane of *interior* vertices and marches along x (the slowest index),
-// staging the tile + 1-vertex halo of plane x+1 in a 4-slot shared-memory
-// ring, so every operand value is read from L2 about once.  Boundary vertices
-// (any coordinate 0 or n, ~6/n of the grid) are handled by extra CTAs from a
-// precomputed index list with the per-class weight table.
+// plane of *interior* vertices over TI consecutive x-planes (x is the slowest
+// index) and stages the whole (TI+2) x (TJ+2) x (TK+2) operand tile in shared
+// memory at once (cp.async, zero-fill outside the box), so every operand value
+// is read from L2 about once; each thread then computes its TI vertices along
+// x.  Boundary vertices (any coordinate 0 or n, ~6/n of the grid) are handled
+// by extra CTAs from a precomputed index list with the per-class weight table.
+// (A CTA marching along x through a cp.async ring was built first and measured
+// slower; so were persistent TMA-fed versions of these tiles.)
 //
 // The staging ("loader") step can transform the operand on its way into
 // shared memory, which is how two passes are fused away:

@@ -52,23 +52,3 @@ def test_collapse_only_with_symmetric_cycles():
     ctx = okg.SchurContext(cfg)
     assert ctx.collapse_level == -1
     ctx.close()
-
-
-@pytest.mark.parametrize("dim,n,min_coarse", [(3, 128, 500), (2, 2048, 500), (2, 90, 2116), (3, 50, 17576)])
-def test_one_launch_packed_matvec_bit_identical(monkeypatch, dim, n, min_coarse):
-    """k_coarse_sym1 (one launch, the last contributor of a row block sums it) against
-    k_coarse_sym + k_coarse_sym_sum, on the collapsed bottom (128^3, 2048^2) and on the
-    packed coarsest inverse (90^2: 46^2 = 2,116 unknowns; 50^3: 26^3 = 17,576): same bits,
-    and the row-block counters re-arm from call to call."""
-    cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, min_coarse_size=min_coarse)
-    monkeypatch.setenv("OKG_COARSE1", "0")
-    two = okg.SchurContext(cfg)
-    monkeypatch.setenv("OKG_COARSE1", "1")
-    one = okg.SchurContext(cfg)
-    rng = np.random.default_rng(7)
-    for _ in range(3):
-        x = rng.uniform(-1, 1, one.n)
-        for kind in (_lib.OP_VCYCLE, _lib.OP_SHAT_INV):
-            assert np.array_equal(one.apply(kind, x), two.apply(kind, x)), kind
-    one.close()
-    two.close()

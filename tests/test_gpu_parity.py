@@ -361,22 +361,6 @@ def test_fused_vcycle_bit_identical(dim, n):
         assert np.array_equal(o[1], outs[0][1]) and np.array_equal(o[2], outs[0][2])
 
 
-@pytest.mark.parametrize("n,k", [(64, 10), (256, 10), (64, 9), (128, 2), (64, 1)])
-def test_two_step_chebyshev_bit_identical(n, k):
-    """okg_cheb2.cuh: two Chebyshev steps per pass (2D) give the one-step results."""
-    cfg = okg.SolverConfig(dim=2, n=n, m=0.0, dt=4e-4, cheby_iters=k, gmres_tol=1e-10, gmres_restart=30)
-    rng = np.random.default_rng(n + k)
-    x = rng.uniform(-1, 1, (n + 1) ** 2)
-    outs = []
-    for fuse in (-1, 4):
-        ctx = okg.SchurContext(cfg, cheb_fuse=fuse)
-        ctx.linearize(okg.seeded_ic(ctx.n, 1, 0.0))
-        outs.append([ctx.apply(kind, x) for kind in (_lib.OP_CHEB_M, _lib.OP_CHEB_A, _lib.OP_SCHUR)])
-        ctx.close()
-    for a, b in zip(*outs):
-        assert np.array_equal(a, b)
-
-
 @pytest.mark.parametrize("dim,n", [(2, 16), (2, 48), (2, 64), (3, 8), (3, 16), (3, 24)])
 def test_ssor_sweeps_bit_exact(dim, n):
     """okg_ssor.cuh: the hyperplane-wavefront SSOR sweeps reproduce the reference's

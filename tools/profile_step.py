@@ -21,9 +21,7 @@ ctx = okg.SchurContext(cfg, tiled_min_n=int(os.environ.get("OKG_TILED", "0")),
                        use_graphs=os.environ.get("OKG_GRAPHS", "1") == "1",
                        mg_fuse=int(os.environ.get("OKG_FUSE", "0")),
                        tail_cluster=int(os.environ.get("OKG_TAILC", "0")),
-                       cheb_fuse=int(os.environ.get("OKG_CHEB2", "0")),
-                       mg_collapse=int(os.environ.get("OKG_COLLAPSE", "0")),
-                       mg_cluster=int(os.environ.get("OKG_CLUSTER", "0")))
+                       mg_collapse=int(os.environ.get("OKG_COLLAPSE", "0")))
 print(f"levels={ctx.level_sizes} tiled={ctx.tiled_levels} tail_start={ctx.tail_start} tail_cluster={ctx.tail_cluster} collapse={ctx.collapse_level}", flush=True)
 ctx.set_state(okg.State(okg.seeded_ic(ctx.n, seed, 0.0), np.zeros(ctx.n)))
 setup = _lib.lib.okg_kernel_launch_count()
