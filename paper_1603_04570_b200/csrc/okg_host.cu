@@ -100,7 +100,6 @@ struct Level {
   HostOp shat;
   bool tiled = false;
   bool fused = false;  // V(2,2) through k_mg_down / k_mg_up (okg_vcycle.cuh)
-  bool rr = false;     // tiled level, one slab: residual + restriction in one launch (okg_rr.cuh)
   Tiling tl{};
   unsigned tl_blocks = 0;
   Tiling tlc{};  // the C-block kernels' tiling (okg_tiled_c.cuh): same tiles, their own x-chunks
@@ -968,18 +967,6 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
   }
   // ---- residual, restriction, coarse correction (multigrid.hpp:106-110)
   Level& C = c->lv[l + 1];
-  if (L.tiled && L.rr) {
-    // residual + restriction in one launch (okg_rr.cuh): r never goes to memory
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_resid_restrict<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)RRGeom<DIM>::SMEM));
-      attr = true;
-    }
-    launch(c, k_resid_restrict<DIM>, rr_grid<DIM>(C.g), RRGeom<DIM>::NT, RRGeom<DIM>::SMEM, L.g, C.g, op,
-           (const double*)cur, rhs, C.b);
-    note(c);
-  } else {
   exchange(c, l, cur);
   if (L.tiled) tiled<DIM, L_PLAIN, T_RESID>(c, L, L.shat, targs(cur, rhs, L.res, nullptr, 0.0));
   else op_apply<DIM>(c, L.g, L.shat, EPI_RESID, cur, rhs, L.res, nullptr);
@@ -991,7 +978,6 @@ static void mg_level(okg_ctx* c, int l, const double* rhs, double* out, bool acc
     launch(c, k_restrict<DIM>, own(gcr), BS, 0, L.g, gcr, (const double*)L.res, C.b);
     note(c);
     if (C.rep && !L.rep) allgather_planes(c, l + 1, C.b);
-  }
   }
   mg_level<DIM>(c, l + 1, C.b, C.x, false);
   // ---- prolongation + post-smoothing (multigrid.hpp:111-115)
@@ -1966,14 +1952,6 @@ static void build(okg_ctx* c) {
     if (tmin > 0)
       for (Level& L : c->lv)
         if (L.g.n >= std::max(tmin, 2)) make_tiling<DIM>(c, L);
-    // fused residual + restriction on tiled levels that are not split across slabs
-    // (environment OKG_RR=0 at okg_create: the two separate kernels, for A/B runs)
-    {
-      const char* e = std::getenv("OKG_RR");
-      const bool want = !(e && std::atoi(e) == 0);
-      for (size_t l = 0; l + 1 < c->lv.size(); ++l)
-        c->lv[l].rr = want && c->lv[l].tiled && S == 1 && (c->lv[l].g.n % 2 == 0);
-    }
     // coarsest: dense SPD inverse (replaces CholeskyFactor, multigrid.hpp:82-83)
     Level& Lc = c->lv.back();
     const int nc = (int)Lc.g.N;

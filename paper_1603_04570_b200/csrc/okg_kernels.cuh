@@ -929,6 +929,5 @@ __global__ void __launch_bounds__(BS) k_check_finite(const double* __restrict__ 
 }  // namespace okg
 
 #include "okg_tiled_c.cuh"
-#include "okg_rr.cuh"
 #include "okg_vcycle.cuh"
 #include "okg_tail.cuh"  // uses slot_ok / op_row above

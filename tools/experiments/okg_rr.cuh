@@ -90,19 +90,34 @@ __global__ void __launch_bounds__(RRGeom<DIM>::NT) k_resid_restrict(Grid gf, Gri
     cp_async8(xs + e, x + (in ? lin : 0u), in);
   }
   cp_commit();
+  // the rhs of this thread's r-region vertices, in flight together with the x tile
+  constexpr int M = (G::RSZ + G::NT - 1) / G::NT;
+  double bv[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int e = tid + m * G::NT;
+    const int pk = e % G::RK, t = e / G::RK;
+    const int pj = DIM == 3 ? t % G::RJ : 0, pi = DIM == 3 ? t / G::RJ : t;
+    const int fi = xi0 + 1 + pi, fj = DIM == 3 ? xj0 + 1 + pj : 0, fk = xk0 + 1 + pk;
+    const bool in = e < G::RSZ && fi >= 0 && fi <= gf.n && fk >= 0 && fk <= gf.n && (DIM == 2 || (fj >= 0 && fj <= gf.n));
+    const uint32_t lin = DIM == 3 ? (uint32_t)fi * gf.ps + (uint32_t)fj * gf.s + fk : (uint32_t)fi * gf.s + fk;
+    bv[m] = in ? b[lin] : 0.0;
+  }
   cp_wait<0>();
   __syncthreads();
   pdl_trigger();
   // ---- 2. r = b - A x on the r region (0 outside the box)
   constexpr int XPS = G::XJ * G::XK;
-  for (int e = tid; e < G::RSZ; e += G::NT) {
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int e = tid + m * G::NT;
+    if (e >= G::RSZ) break;
     const int pk = e % G::RK, t = e / G::RK;
     const int pj = DIM == 3 ? t % G::RJ : 0, pi = DIM == 3 ? t / G::RJ : t;
     const int fi = xi0 + 1 + pi, fj = DIM == 3 ? xj0 + 1 + pj : 0, fk = xk0 + 1 + pk;
     const bool in = fi >= 0 && fi <= gf.n && fk >= 0 && fk <= gf.n && (DIM == 2 || (fj >= 0 && fj <= gf.n));
     double r = 0.0;
     if (in) {
-      const uint32_t lin = DIM == 3 ? (uint32_t)fi * gf.ps + (uint32_t)fj * gf.s + fk : (uint32_t)fi * gf.s + fk;
       const int cls = class_of<DIM>(gf, fi, fj, fk);
       const double* xc = xs + (pi + 1) * XPS + (DIM == 3 ? (pj + 1) * G::XK : 0) + pk + 1;
       double As = 0.0;
@@ -121,7 +136,7 @@ __global__ void __launch_bounds__(RRGeom<DIM>::NT) k_resid_restrict(Grid gf, Gri
           As = fma(__ldg(w + o), xc[di * XPS + dj * G::XK + dk], As);
         }
       }
-      r = b[lin] - As;
+      r = bv[m] - As;
     }
     rs[e] = r;
   }
