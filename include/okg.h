@@ -92,6 +92,11 @@ typedef struct okg_params {
                                the latency-bound bottom of each V-cycle is one HBM-streaming
                                matvec; 0 = default (3D 1000, 2D 1100: the cluster tail's levels),
                                < 0 = never */
+  int64_t rep_max_vertices; /* slab decomposition: levels below the finest with at most this many
+                               vertices (in total) are replicated on every slab instead of split --
+                               a whole small level is cheaper than a share of it plus a ghost-plane
+                               exchange per sweep (cost model in DESIGN.md section 7);
+                               0 = default (3,000,000), < 0 = split as deep as 2 planes per slab */
 } okg_params;
 
 /* ---- okflow::IterationStats (model.hpp:32-42) -------------------------------- */
@@ -192,8 +197,8 @@ int okg_create_rank(const okg_params* p, int32_t rank, int32_t nranks, const voi
  * hierarchy, first level replicated on every slab, and the owned planes [lo[l], hi[l])
  * of `rank` on every level (all planes on replicated levels); lo/hi hold 32 entries */
 int okg_slab_partition(int32_t dim, int32_t n, int32_t min_coarse_size, int32_t nslabs,
-                       int32_t rank, int32_t* levels, int32_t* rep_level, int32_t* lo,
-                       int32_t* hi);
+                       int32_t rank, int64_t rep_max_vertices /* okg_params' */, int32_t* levels,
+                       int32_t* rep_level, int32_t* lo, int32_t* hi);
 
 /* build_mesh arrays, bit-exact (mesh.hpp:87-157); host memory.
  * vertices: N*dim doubles; cells: (2n^2 | 6n^3)*(dim+1) int32 */

@@ -78,7 +78,7 @@ class SolverConfig:
                   tiled_min_n: int = 0, tail_max_vertices: int = 0, pdl: bool = True,
                   mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
                   tail_cluster: int = 0, coarse_split: int = 0,
-                  mg_collapse: int = 0) -> _lib.Params:
+                  mg_collapse: int = 0, rep_max_vertices: int = 0) -> _lib.Params:
         p = _lib.Params()
         lib.okg_default_params(C.byref(p))
         for name in ("dim", "n", "eps", "sigma", "m", "theta", "dt", "newton_tol", "newton_maxit",
@@ -97,6 +97,7 @@ class SolverConfig:
         p.tail_cluster = tail_cluster
         p.coarse_split = coarse_split
         p.mg_collapse = mg_collapse
+        p.rep_max_vertices = rep_max_vertices
         p.cheby_ssor = 1 if self.cheby_precond == "ssor" else 0
         return p
 
@@ -199,13 +200,16 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def slab_partition(dim: int, n: int, nslabs: int, rank: int, min_coarse_size: int = 500):
+def slab_partition(dim: int, n: int, nslabs: int, rank: int, min_coarse_size: int = 500,
+                   rep_max_vertices: int = 0):
     """The slab partition the contexts use (okg_slab_partition): returns
-    (levels, rep_level, [(lo, hi) owned x-planes per level])."""
+    (levels, rep_level, [(lo, hi) owned x-planes per level]).  rep_max_vertices as in
+    okg_params (0 = default 3,000,000, < 0 = split as deep as 2 planes per slab)."""
     lv, rep = C.c_int32(), C.c_int32()
     lo = (C.c_int32 * 32)()
     hi = (C.c_int32 * 32)()
-    check(lib.okg_slab_partition(dim, n, min_coarse_size, nslabs, rank, C.byref(lv), C.byref(rep), lo, hi))
+    check(lib.okg_slab_partition(dim, n, min_coarse_size, nslabs, rank, C.c_int64(rep_max_vertices),
+                                 C.byref(lv), C.byref(rep), lo, hi))
     return lv.value, rep.value, [(lo[l], hi[l]) for l in range(lv.value)]
 
 
@@ -305,7 +309,8 @@ class SchurContext:
                  use_graphs: bool = True, tiled_min_n: int = 0, tail_max_vertices: int = 0,
                  pdl: bool = True, mg_fuse: int = 0, nslabs: int = 1, slab_devices: bool = False,
                  rank: Optional[int] = None, nranks: int = 1, nccl_id: Optional[bytes] = None,
-                 tail_cluster: int = 0, coarse_split: int = 0, mg_collapse: int = 0):
+                 tail_cluster: int = 0, coarse_split: int = 0, mg_collapse: int = 0,
+                 rep_max_vertices: int = 0):
         """nslabs > 1: x-plane slab decomposition, one host thread + stream per
         slab, all on `device` (slab_devices=False, the 1-GPU emulation) or slab r on device
         `device + r`.  rank/nranks/nccl_id: one process per GPU (okg_create_rank), this
@@ -315,7 +320,8 @@ class SchurContext:
         self.device = device
         self.handle = C.c_void_p()
         params = cfg.to_params(device, shat_perturb, use_graphs, tiled_min_n, tail_max_vertices, pdl, mg_fuse,
-                               nslabs, slab_devices, tail_cluster, coarse_split, mg_collapse)
+                               nslabs, slab_devices, tail_cluster, coarse_split, mg_collapse,
+                               rep_max_vertices)
         if rank is None:
             check(lib.okg_create(C.byref(params), C.byref(self.handle)))
         else:

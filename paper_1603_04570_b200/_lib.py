@@ -50,6 +50,7 @@ class Params(C.Structure):
         ("cheby_ssor", C.c_int32),
         ("coarse_split", C.c_int32),
         ("mg_collapse", C.c_int32),
+        ("rep_max_vertices", C.c_int64),
     ]
 
 
@@ -158,7 +159,7 @@ _SIGS = {
     "okg_initial_state": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "okg_advance": (C.c_int, [_vp, C.c_int32, C.POINTER(StepStats)]),
     "okg_create_rank": (C.c_int, [C.POINTER(Params), C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
-    "okg_slab_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+    "okg_slab_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32)]),
     "okg_linearize_host": (C.c_int, [_vp, _dp]),

@@ -452,7 +452,16 @@ static void allgather_planes(okg_ctx* c, int l, double* x) {
 // (and always the coarsest), levels are replicated on every slab.  Writes the
 // owned planes [lo[l], hi[l]) of `rank` for every split level and returns the
 // first replicated level.  s0 = planes of the finest level, nlev = levels.
-static int slab_partition(int s0, int nlev, int S, int rank, int* lo, int* hi) {
+// A level is replicated (every slab holds and computes all of it) from the first level
+// where some slab would keep fewer than 2 planes, from the first level below the finest
+// with at most rep_max vertices in total, and always on the coarsest level.  The vertex
+// rule is a cost model: one sweep of a whole level of N vertices costs
+// max(4 us, N * 24 B / 5 TB/s) on one B200, a sweep of a 1/S share costs the share's
+// time plus ~12 us for the ghost-plane exchange, so replicating wins below ~3 M vertices
+// whatever S is.
+static int64_t rep_max_default() { return 3000000; }
+static int64_t rep_max_of(const okg_params& p) { return p.rep_max_vertices == 0 ? rep_max_default() : p.rep_max_vertices; }
+static int slab_partition(int dim, int s0, int nlev, int S, int rank, int64_t rep_max, int* lo, int* hi) {
   auto fine = [&](int r, int& a, int& b) {
     a = 2 * (int)(((long)r * s0) / (2L * S));
     b = r == S - 1 ? s0 : 2 * (int)(((long)(r + 1) * s0) / (2L * S));
@@ -470,6 +479,8 @@ static int slab_partition(int s0, int nlev, int S, int rank, int* lo, int* hi) {
       }
       minp = std::min(minp, rb - ra);
     }
+    const int64_t sl = (int64_t)((s0 - 1) >> l) + 1, Nl = dim == 2 ? sl * sl : sl * sl * sl;
+    if (l > 0 && rep_max > 0 && Nl <= rep_max) return l;
     if (minp < 2 || l + 1 == nlev) return l;
     lo[l] = a;
     hi[l] = b;
@@ -1852,7 +1863,7 @@ static void build(okg_ctx* c) {
     c->L_rep = (int)c->lv.size();
     if (S > 1) {
       std::vector<int> lo(c->lv.size()), hi(c->lv.size());
-      c->L_rep = slab_partition(c->lv[0].g.s, (int)c->lv.size(), S, c->rank, lo.data(), hi.data());
+      c->L_rep = slab_partition(DIM, c->lv[0].g.s, (int)c->lv.size(), S, c->rank, rep_max_of(p), lo.data(), hi.data());
       if (c->L_rep == 0) THROW(OKG_EINVAL, "slab decomposition: %d slabs leave fewer than 2 planes each", S);
       for (int l = 0; l < c->L_rep; ++l) {
         set_owned(c->lv[l].g, lo[l], hi[l]);
@@ -1864,7 +1875,7 @@ static void build(okg_ctx* c) {
       c->rep_hi.assign(S, 0);
       for (int r = 0; r < S; ++r) {
         std::vector<int> rl(c->lv.size()), rh(c->lv.size());
-        slab_partition(c->lv[0].g.s, (int)c->lv.size(), S, r, rl.data(), rh.data());
+        slab_partition(DIM, c->lv[0].g.s, (int)c->lv.size(), S, r, rep_max_of(p), rl.data(), rh.data());
         c->rep_lo[r] = (rl[c->L_rep - 1] + 1) / 2;
         c->rep_hi[r] = (rh[c->L_rep - 1] + 1) / 2;
       }
@@ -2609,7 +2620,7 @@ int okg_create_rank(const okg_params* p, int32_t rank, int32_t nranks, const voi
 }
 
 int okg_slab_partition(int32_t dim, int32_t n, int32_t min_coarse_size, int32_t nslabs, int32_t rank,
-                       int32_t* levels, int32_t* rep_level, int32_t* lo, int32_t* hi) {
+                       int64_t rep_max_vertices, int32_t* levels, int32_t* rep_level, int32_t* lo, int32_t* hi) {
   if ((dim != 2 && dim != 3) || n < 1 || min_coarse_size < 1 || nslabs < 1 || rank < 0 || rank >= nslabs || !levels ||
       !rep_level || !lo || !hi)
     return fail(OKG_EINVAL, "okg_slab_partition: bad argument");
@@ -2625,7 +2636,8 @@ int okg_slab_partition(int32_t dim, int32_t n, int32_t min_coarse_size, int32_t 
   for (int l = 0; l < nlev; ++l) h0[l] = (n >> l) + 1;  // one slab / replicated level: every plane
   int rep = nlev;
   if (nslabs > 1) {
-    rep = slab_partition(n + 1, nlev, nslabs, rank, l0.data(), h0.data());
+    rep = slab_partition(dim, n + 1, nlev, nslabs, rank, rep_max_vertices == 0 ? rep_max_default() : rep_max_vertices,
+                         l0.data(), h0.data());
     if (rep == 0) return fail(OKG_EINVAL, "slab decomposition: %d slabs leave fewer than 2 planes each", nslabs);
     for (int l = rep; l < nlev; ++l) {
       l0[l] = 0;
@@ -2680,7 +2692,7 @@ int okg_get_info(okg_ctx* h, okg_info* info) {
   for (int r = 0; r < info->nslabs; ++r) {
     std::vector<int> lo(c->lv.size()), hi(c->lv.size());
     if (info->nslabs > 1) {
-      slab_partition(c->lv[0].g.s, (int)c->lv.size(), info->nslabs, r, lo.data(), hi.data());
+      slab_partition(c->dim, c->lv[0].g.s, (int)c->lv.size(), info->nslabs, r, rep_max_of(c->p), lo.data(), hi.data());
     } else {
       lo[0] = 0;
       hi[0] = c->lv[0].g.s;

@@ -36,7 +36,10 @@ ROUNDING = [("CHEB_M", _lib.OP_CHEB_M), ("CHEB_A", _lib.OP_CHEB_A), ("SCHUR", _l
 
 MODES = {"default": {}, "tiled": dict(tiled_min_n=2, mg_fuse=1), "plain": dict(tiled_min_n=-1, mg_fuse=-1)}
 
-CASES = [(2, 64, 2), (2, 64, 3), (2, 128, 4), (3, 16, 2), (3, 32, 3), (3, 32, 4)]
+# (dim, n, slabs, rep_max_vertices): -1 splits every level down to 2 planes per slab (the deep
+# hierarchy of ghost exchanges), 0 is the default cost-model rule (small levels replicated)
+CASES = [(2, 64, 2, -1), (2, 64, 3, -1), (2, 128, 4, -1), (3, 16, 2, -1), (3, 32, 3, -1), (3, 32, 4, -1),
+         (2, 128, 4, 0), (3, 32, 4, 0), (3, 32, 2, 2000)]
 
 
 def cfg_for(dim, n):
@@ -45,14 +48,15 @@ def cfg_for(dim, n):
 
 
 @pytest.fixture(scope="module", params=[(c, m) for c in CASES for m in MODES],
-                ids=lambda p: f"{p[0][0]}d{p[0][1]}-s{p[0][2]}-{p[1]}")
+                ids=lambda p: f"{p[0][0]}d{p[0][1]}-s{p[0][2]}-r{p[0][3]}-{p[1]}")
 def pair(request):
-    (dim, n, S), mode = request.param
+    (dim, n, S, rep_max), mode = request.param
     cfg = cfg_for(dim, n)
     # the collapsed bottom of the V-cycle needs whole (replicated) levels; a split level
     # would keep the recursive cycle on the slabs -- compare like with like
     one = okg.SchurContext(cfg, mg_collapse=-1, **MODES[mode])
-    many = okg.SchurContext(cfg, nslabs=S, mg_collapse=-1, **MODES[mode])
+    many = okg.SchurContext(cfg, nslabs=S, mg_collapse=-1, rep_max_vertices=rep_max, **MODES[mode])
+    many.rep_max = rep_max
     yield dim, n, S, one, many
     many.close()
     one.close()

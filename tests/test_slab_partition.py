@@ -18,7 +18,10 @@ CASES = [(2, 64, 2), (2, 64, 3), (2, 128, 4), (2, 2048, 8), (2, 2944, 2), (2, 58
          (3, 128, 2), (3, 128, 8), (3, 160, 2), (3, 192, 4), (3, 256, 8)]
 
 
-def restated(dim, n, S, rank, mcs=500):
+REP_MAX = 3_000_000  # okg_params.rep_max_vertices default
+
+
+def restated(dim, n, S, rank, mcs=500, rep_max=REP_MAX):
     """The partition rule in plain Python."""
     sizes, ln = [], n
     while True:
@@ -37,7 +40,8 @@ def restated(dim, n, S, rank, mcs=500):
     ranges = [fine(r) for r in range(S)]
     rep, out = nlev, []
     for l in range(nlev):
-        if min(b - a for a, b in ranges) < 2 or l + 1 == nlev:
+        small = l > 0 and rep_max > 0 and (sizes[l] + 1) ** dim <= rep_max
+        if small or min(b - a for a, b in ranges) < 2 or l + 1 == nlev:
             rep = l
             break
         out.append(ranges[rank])
@@ -46,15 +50,29 @@ def restated(dim, n, S, rank, mcs=500):
     return nlev, rep, out
 
 
+@pytest.mark.parametrize("rep_max", [0, -1, 40000])
 @pytest.mark.parametrize("dim,n,S", CASES)
-def test_partition_matches_rule(dim, n, S):
+def test_partition_matches_rule(dim, n, S, rep_max):
     for r in range(S):
-        assert okg.slab_partition(dim, n, S, r) == restated(dim, n, S, r)
+        assert okg.slab_partition(dim, n, S, r, rep_max_vertices=rep_max) == \
+            restated(dim, n, S, r, rep_max=REP_MAX if rep_max == 0 else rep_max)
 
 
+def test_replication_threshold_on_baseline_meshes():
+    """The cost-model rule on the BASELINE meshes: configs[3] (128^3 on 8 slabs) keeps only the
+    finest level split; configs[4] (800^3 on 8) splits 801^3, 401^3, 201^3 and replicates from
+    101^3 (1.03 M vertices) down; the old rule (rep_max < 0) splits down to 2 planes per slab."""
+    assert okg.slab_partition(3, 128, 8, 0)[1] == 1
+    assert okg.slab_partition(3, 128, 8, 0, rep_max_vertices=-1)[1] == 4
+    assert okg.slab_partition(3, 800, 8, 3, min_coarse_size=17576)[1] == 3
+    assert okg.slab_partition(3, 800, 8, 3, min_coarse_size=17576, rep_max_vertices=-1)[1] == 5
+    assert okg.slab_partition(2, 2048, 8, 0)[1] == 1  # 1025^2 = 1.05 M vertices: replicated
+
+
+@pytest.mark.parametrize("rep_max", [0, -1])
 @pytest.mark.parametrize("dim,n,S", CASES)
-def test_partition_tiles_and_nests(dim, n, S):
-    parts = [okg.slab_partition(dim, n, S, r) for r in range(S)]
+def test_partition_tiles_and_nests(dim, n, S, rep_max):
+    parts = [okg.slab_partition(dim, n, S, r, rep_max_vertices=rep_max) for r in range(S)]
     nlev, rep = parts[0][0], parts[0][1]
     assert 1 <= rep <= nlev - 1
     for l in range(nlev):
