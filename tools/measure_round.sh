@@ -11,11 +11,6 @@ timeout 900 python bench.py --impl reference > gpurun_out/${P}_bench_ref.json 2>
 bash tools/launch_list.sh ${P}_3d128 3 128 > /dev/null 2>&1
 OKG_MIN_COARSE=17576 bash tools/launch_list.sh ${P}_3d400 3 400 > /dev/null 2>&1
 bash tools/launch_list.sh ${P}_2d2048 2 2048 > /dev/null 2>&1
-KREGEX="k_tiled" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 128 5 1" bash tools/ncu_full.sh ${P}_resid128 > /dev/null 2>&1
-OKG_MIN_COARSE=17576 KREGEX="k_tiled" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 400 5 1" bash tools/ncu_full.sh ${P}_resid400 > /dev/null 2>&1
-for f in ${P}_resid128 ${P}_resid400; do
-  ncu -i gpurun_out/$f.ncu-rep --page raw --csv > gpurun_out/${f}_raw.csv 2>/dev/null
-  ncu -i gpurun_out/$f.ncu-rep --page details --csv > gpurun_out/${f}_details.csv 2>/dev/null
-done
+bash tools/ncu_kernels.sh ${P}
 for f in gpurun_out/${P}_bench_*.json; do echo $f; tail -c 400 $f; echo; done
 head -12 gpurun_out/ll_${P}_3d128.summary.txt gpurun_out/ll_${P}_3d400.summary.txt gpurun_out/ll_${P}_2d2048.summary.txt

@@ -4,6 +4,6 @@
 set -u
 mkdir -p gpurun_out
 $CMD > gpurun_out/ncu_plain_$1.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${KREGEX}" -s ${SKIP:-3} -c ${COUNT:-1} \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base ${KBASE:-function} -k "regex:${KREGEX}" -s ${SKIP:-3} -c ${COUNT:-1} \
   -o gpurun_out/$1 $CMD > gpurun_out/ncu_$1.log 2>&1
 echo "ncu rc=$?"; tail -3 gpurun_out/ncu_$1.log
