@@ -99,6 +99,7 @@ struct Level {
   bool rep = false; // replicated on every slab (levels too thin to split, the coarsest)
   HostOp shat;
   bool tiled = false;
+  bool wide = false;   // tiled plain-load kernels stage in 16-byte chunks (k_tiled WIDE; odd row pitch)
   bool fused = false;  // V(2,2) through k_mg_down / k_mg_up (okg_vcycle.cuh)
   Tiling tl{};
   unsigned tl_blocks = 0;
@@ -577,20 +578,33 @@ static void op_apply(okg_ctx* c, const Grid& g, const HostOp& op, int epi, const
 #endif
 constexpr int SMEM_CARVEOUT = OKG_CARVEOUT;
 
-template <int DIM, int LOAD, int EPI, int TI>
-static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
+template <int DIM, int LOAD, int EPI, int TI, int WIDE>
+static void tiled_tw(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
   static bool attr = false;  // dynamic smem above 48 KB needs an opt-in (per kernel instance)
-  const size_t smem = tiled_smem_bytes<DIM, LOAD, TI>();
+  const size_t smem = tiled_smem_bytes<DIM, LOAD, TI, WIDE>();
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // half of the unified L1/shared array as shared memory: the tiles of 4 CTAs fit, and
     // the rest stays L1 for the cp.async (.ca) and pointwise loads -- measured at 400^3:
     // carveout 100 -> 430 us, 50 -> 267 us per fine-level sweep (30: 320 us)
-    CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI>, cudaFuncAttributePreferredSharedMemoryCarveout, SMEM_CARVEOUT));
+    CK(cudaFuncSetAttribute(k_tiled<DIM, LOAD, EPI, TI, WIDE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            SMEM_CARVEOUT));
     attr = true;
   }
-  launch(c, k_tiled<DIM, LOAD, EPI, TI>, L.tl_blocks, TileCfg<DIM>::NT, smem, L.g, dev_op<DIM>(op), L.tl, a);
+  launch(c, k_tiled<DIM, LOAD, EPI, TI, WIDE>, L.tl_blocks, TileCfg<DIM>::NT, smem, L.g, dev_op<DIM>(op), L.tl, a);
   note(c);
+}
+
+// 16-byte staging (k_tiled's WIDE) for the plain-load kernels of levels with an odd row pitch
+template <int DIM, int LOAD, int EPI, int TI>
+static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
+  if constexpr (LOAD == L_PLAIN && (TI == 8 || TI == 4)) {
+    if (L.wide) {
+      tiled_tw<DIM, LOAD, EPI, TI, 1>(c, L, op, a);
+      return;
+    }
+  }
+  tiled_tw<DIM, LOAD, EPI, TI, 0>(c, L, op, a);
 }
 
 template <int DIM, int LOAD, int EPI>
@@ -666,6 +680,11 @@ static void make_tiling(okg_ctx* c, Level& L) {
     }
     t.ichunk = best;
     t.ncore = base * ((nci + best - 1) / best);
+  }
+  t.vend = (uint32_t)(L.g.ihi + L.gh) * L.g.ps;
+  {
+    const char* e = std::getenv("OKG_WIDE");  // A/B: OKG_WIDE=0 keeps the 8-byte staging
+    L.wide = (L.g.s & 1) && !(e && std::atoi(e) == 0);
   }
   double* d = dalloc(c, (bnd.size() + 1) / 2 + 1);
   CK(cudaMemcpyAsync(d, bnd.data(), bnd.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));

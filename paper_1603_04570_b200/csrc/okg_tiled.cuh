@@ -48,6 +48,7 @@ struct Tiling {
   int32_t ktiles, jtiles, ichunk;  // tiles along z, y; planes per CTA along x (= TI)
   int32_t ci0, ci1;  // interior planes [ci0, ci1) of this slab handled by core CTAs
   uint32_t nbnd;    // boundary vertices
+  uint32_t vend;    // end of a level vector's index range (owned + ghost planes): 16-byte staging clamps there
   const uint32_t* __restrict__ bnd;  // boundary vertex indices
 };
 
@@ -77,10 +78,12 @@ struct CoarseTile {
   static constexpr int SIZE = CI * CJ * CK;
 };
 
-template <int DIM, int LOAD, int TI>
+// WIDE: tile rows of PW + 2 doubles staged in 16-byte chunks (see k_tiled)
+template <int DIM, int LOAD, int TI, int WIDE = 0>
 constexpr size_t tiled_smem_bytes() {
   // (TI >= 4 only: on thin tiles the extra pass costs more than the loads it saves)
-  return sizeof(double) * ((size_t)(TI + 2) * TileCfg<DIM>::PSZ + (LOAD == 2 && TI >= 4 ? CoarseTile<DIM, TI>::SIZE : 0));
+  return sizeof(double) * ((size_t)(TI + 2) * (TileCfg<DIM>::PSZ / TileCfg<DIM>::PW) * (TileCfg<DIM>::PW + (WIDE ? 2 : 0)) +
+                           (LOAD == 2 && TI >= 4 ? CoarseTile<DIM, TI>::SIZE : 0));
 }
 
 struct TArgs {
@@ -99,6 +102,10 @@ struct TArgs {
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
+}
+// 16-byte cp.async (LDGSTS.128) to a shared-window address, zero-filled when !valid
+__device__ __forceinline__ void cp_async16(unsigned sdst, const double* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -230,11 +237,25 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
 // Core CTAs: a (TI+2) x (TJ+2) x (TK+2) tile (3D) or (TI+2) x (TK+2) (2D) of
 // staged values is loaded with all global loads in flight at once, then each
 // thread computes TI vertices along x.  Extra CTAs take the boundary list.
-template <int DIM, int LOAD, int EPI, int TI>
+//
+// WIDE (plain loads only; levels with an odd row pitch s, i.e. every level that coarsens):
+// the shared-memory side of the 8-byte LDGSTS staging is a quarter of the L1 data-pipe
+// wavefronts that bound these kernels.  A tile row is not 16-byte
+// aligned in the reference's vertex order (s odd), so each row of PW doubles is fetched as
+// PW/2 + 1 16-byte chunks from its address rounded DOWN to 16 bytes into a row of RP = PW + 2
+// doubles: element hk of row (p, hj) then sits at row * RP + par + hk with par = the address
+// parity of the row start = a00 ^ ((p + hj) & 1) (s and s^2 odd) -- in the unrolled tap loop a
+// compile-time choice between two per-thread base pointers, no instruction per tap.  Half the
+// copies, half their shared-memory wavefronts, bit-identical results.
+template <int DIM, int LOAD, int EPI, int TI, int WIDE = 0>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
   pdl_wait();  // (the dependent grid is released below, once the tile is staged)
   using TC = TileCfg<DIM>;
+  static_assert(!WIDE || LOAD == L_PLAIN, "16-byte staging: plain loads only");
   constexpr int NO = Traits<DIM>::NOFF;
+  constexpr int PHT = TC::PSZ / TC::PW;             // rows per staged plane (1 in 2D)
+  constexpr int RP = WIDE ? TC::PW + 2 : TC::PW;    // shared-memory row pitch
+  constexpr int PSZ = PHT * RP;                     // doubles per staged plane
   const int tid = threadIdx.x;
   // boundary CTAs come first: their gathers are the longest path of the kernel,
   // so they should overlap the core tiles instead of forming its tail
@@ -245,7 +266,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     return;
   }
   // ---- core tile ----
-  extern __shared__ double tile[];
+  extern __shared__ __align__(16) double tile[];
   int b = (int)blockIdx.x - nbb;
   const int kt = b % tl.ktiles;
   b /= tl.ktiles;
@@ -278,7 +299,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   }
   // L_PROLONG: coarse tile covering the fine planes/rows/columns of the staged tile
   using CT = CoarseTile<DIM, TI>;
-  double* ct = tile + (TI + 2) * TC::PSZ;
+  double* ct = tile + (TI + 2) * PSZ;
   const int cbi = (i0 - 1) >> 1, cbj = DIM == 3 ? (j0 - 1) >> 1 : 0, cbk = (k0 - 1) >> 1;
   constexpr bool CSTAGE = LOAD == L_PROLONG && TI >= 4;
   if (CSTAGE) {
@@ -313,7 +334,45 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   // issue order (measured, A/B on one box): per plane for the transformed loads and the
   // Chebyshev step, in linear tile order for the plain sweeps (5 % either way)
   constexpr bool PLANE_ISSUE = LOAD != L_PLAIN || EPI == T_CHEB;
-  if (PLANE_ISSUE) {
+  // (WIDE) linear index of staged element (plane i0-1, row j0-1, column k0-1) and its address parity
+  const uint32_t lin0 = (uint32_t)(i0 - 1) * pstride + (DIM == 3 ? (uint32_t)(j0 - 1) * g.s : 0u) + (uint32_t)(k0 - 1);
+  const int a00 = WIDE ? (int)((reinterpret_cast<uintptr_t>(a.x + lin0) >> 3) & 1u) : 0;
+  if constexpr (WIDE) {
+    // 16-byte chunks in linear order: chunk e = tid + m NT is chunk c = e % CH of row r = e / CH
+    // and lands at tile + 2 e (RP = 2 CH); (p, hj, c) advance incrementally (NT = DR CH + DC,
+    // DR = DP PHT + DH: at most one carry each)
+    constexpr int CH = RP / 2, DR = TC::NT / CH, DC = TC::NT % CH, DP = DR / PHT, DH = DR % PHT;
+    static_assert(RP % 2 == 0 && DH + 1 <= PHT, "one carry per step");
+    const int total = (ni + 2) * PHT * CH;
+    int r0 = tid / CH, c = tid - r0 * CH;
+    int p = DIM == 3 ? r0 / PHT : r0, hj = DIM == 3 ? r0 - p * PHT : 0;
+    const int jmax = DIM == 3 ? g.n - (j0 - 1) : 0;
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(tile));
+    for (int e = tid; e < total; e += TC::NT) {
+      const uint32_t lin = lin0 + (uint32_t)p * pstride + (DIM == 3 ? (uint32_t)hj * (uint32_t)g.s : 0u) + 2u * (uint32_t)c;
+      const uint32_t par = (uint32_t)(a00 ^ ((p + hj) & 1));
+      const bool ok = hj <= jmax && lin < tl.vend + par;  // chunk start lin - par inside the vector
+      // (pointer arithmetic, not index arithmetic: lin - par wraps for the first element of a vector
+      // that starts 8 bytes into a 16-byte chunk, e.g. the w half of a stacked [u; w])
+      cp_async16(sbase + (unsigned)e * 16u, ok ? (a.x + lin) - par : (a.x + lin0) - a00, ok);
+      c += DC;
+      int dr = DR;
+      if (c >= CH) {
+        c -= CH;
+        dr += 1;
+      }
+      if (DIM == 3) {
+        hj += dr - DP * PHT;
+        p += DP;
+        if (hj >= PHT) {
+          hj -= PHT;
+          p += 1;
+        }
+      } else {
+        p += dr;
+      }
+    }
+  } else if (PLANE_ISSUE) {
 #pragma unroll
     for (int p = 0; p < TI + 2; ++p) {
       if (p < ni + 2) {
@@ -446,6 +505,11 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   // their dependent FMA chains interleave); only the stores are predicated
   // JAC0: taps scaled by scl (wd on folded tiles, else 1.0 -- exact)
   const double scl = fold ? a.omega * op.invd : 1.0;
+  // this thread's centre column in rows whose (plane + row) parity equals / differs from its
+  // own row's: one pointer without WIDE, two (shifted by the rows' address parity) with it
+  const int q0 = DIM == 3 ? (tj & 1) : 1;
+  const double* tE = tile + (DIM == 3 ? (tj + 1) * RP : 0) + tk + 1 + (WIDE ? (a00 ^ q0) : 0);
+  const double* tO = tile + (DIM == 3 ? (tj + 1) * RP : 0) + tk + 1 + (WIDE ? (a00 ^ q0 ^ 1) : 0);
 #pragma unroll
   for (int t = 0; t < TI; ++t) {
     double As = 0.0, s_own = 0.0, raw_own = 0.0;
@@ -454,7 +518,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       const int di = off_comp(DIM, o, 0);
       const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
       const int dk = off_comp(DIM, o, DIM - 1);
-      const double raw = tile[(t + 1 + di) * TC::PSZ + (DIM == 3 ? (tj + 1 + dj) * TC::PW : 0) + tk + 1 + dk];
+      const double raw = (((t + di + dj) & 1) ? tO : tE)[(t + 1 + di) * PSZ + (DIM == 3 ? dj * RP : 0) + dk];
       const double sv = (OKG_JAC0_FOLD && LOAD == L_JAC0) ? scl * raw : raw;
       if (o == Traits<DIM>::CENTER) {
         s_own = sv;

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(TK* TJT, MINB) v_tile(G3 g, W15 cw, const doub
       const uint32_t lin = lin0 + (uint32_t)p * g.ps + (uint32_t)hj * g.s + 2u * c;
       const uint32_t par = (uint32_t)(a00 ^ ((p + hj) & 1));
       const bool in = j0 - 1 + hj <= g.n && lin < vend + par;
-      cp16(sbase + (unsigned)e * 16u, x + (in ? lin - par : lin0 - a00), in);
+      cp16(sbase + (unsigned)e * 16u, in ? (x + lin) - par : (x + lin0) - a00, in);
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
