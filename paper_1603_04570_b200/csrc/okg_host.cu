@@ -99,7 +99,9 @@ struct Level {
   bool rep = false; // replicated on every slab (levels too thin to split, the coarsest)
   HostOp shat;
   bool tiled = false;
-  bool wide = false;   // tiled plain-load kernels stage in 16-byte chunks (k_tiled WIDE; odd row pitch)
+  bool wide = false;   // tiled kernels stage in 16-byte chunks (k_tiled WIDE; odd row pitch)
+  bool wide_xf = false;  // ... also the kernels with a staging transform (L_JAC0; L_PROLONG in 2D)
+  bool wide_thin = false;  // ... also on levels whose tiles are 2 or 3 planes thick
   bool fused = false;  // V(2,2) through k_mg_down / k_mg_up (okg_vcycle.cuh)
   Tiling tl{};
   unsigned tl_blocks = 0;
@@ -598,8 +600,11 @@ static void tiled_tw(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& 
 // 16-byte staging (k_tiled's WIDE) for the plain-load kernels of levels with an odd row pitch
 template <int DIM, int LOAD, int EPI, int TI>
 static void tiled_ti(okg_ctx* c, const Level& L, const HostOp& op, const TArgs& a) {
-  if constexpr (LOAD == L_PLAIN && (TI == 8 || TI == 4)) {
-    if (L.wide) {
+  // (the Chebyshev step measured no faster with it: 128^3 18.1 vs 18.5 us, 400^3 546 vs 554 us)
+  // and the prolongation-staged sweep in 3D slower: 400^3 467 vs 442 us; pre-sweep kernel 289 vs 303 us,
+  // 2D: pre-sweeps 13.9 vs 15.6 us, prolongation sweep 20.1 vs 23.2 us)
+  if constexpr (EPI != T_CHEB && !(LOAD == L_PROLONG && (TI < 4 || DIM == 3))) {
+    if (L.wide && (LOAD == L_PLAIN || L.wide_xf) && (TI >= 4 || L.wide_thin)) {
       tiled_tw<DIM, LOAD, EPI, TI, 1>(c, L, op, a);
       return;
     }
@@ -683,8 +688,10 @@ static void make_tiling(okg_ctx* c, Level& L) {
   }
   t.vend = (uint32_t)(L.g.ihi + L.gh) * L.g.ps;
   {
-    const char* e = std::getenv("OKG_WIDE");  // A/B: OKG_WIDE=0 keeps the 8-byte staging
+    const char* e = std::getenv("OKG_WIDE");  // A/B at okg_create: OKG_WIDE=0 keeps the 8-byte staging
     L.wide = (L.g.s & 1) && !(e && std::atoi(e) == 0);
+    L.wide_xf = L.wide && !(e && std::atoi(e) == 1);  // A/B: OKG_WIDE=1 plain-load kernels only
+    L.wide_thin = L.wide && !(e && std::atoi(e) == 2);  // A/B: OKG_WIDE=2 tiles of 4 and 8 planes only
   }
   double* d = dalloc(c, (bnd.size() + 1) / 2 + 1);
   CK(cudaMemcpyAsync(d, bnd.data(), bnd.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));

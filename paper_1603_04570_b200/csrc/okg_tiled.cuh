@@ -251,7 +251,7 @@ template <int DIM, int LOAD, int EPI, int TI, int WIDE = 0>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
   pdl_wait();  // (the dependent grid is released below, once the tile is staged)
   using TC = TileCfg<DIM>;
-  static_assert(!WIDE || LOAD == L_PLAIN, "16-byte staging: plain loads only");
+  static_assert(!(WIDE && LOAD == L_PROLONG && TI < 4), "16-byte staging of the prolongation needs the coarse tile");
   constexpr int NO = Traits<DIM>::NOFF;
   constexpr int PHT = TC::PSZ / TC::PW;             // rows per staged plane (1 in 2D)
   constexpr int RP = WIDE ? TC::PW + 2 : TC::PW;    // shared-memory row pitch
@@ -337,24 +337,33 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   // (WIDE) linear index of staged element (plane i0-1, row j0-1, column k0-1) and its address parity
   const uint32_t lin0 = (uint32_t)(i0 - 1) * pstride + (DIM == 3 ? (uint32_t)(j0 - 1) * g.s : 0u) + (uint32_t)(k0 - 1);
   const int a00 = WIDE ? (int)((reinterpret_cast<uintptr_t>(a.x + lin0) >> 3) & 1u) : 0;
-  if constexpr (WIDE) {
-    // 16-byte chunks in linear order: chunk e = tid + m NT is chunk c = e % CH of row r = e / CH
-    // and lands at tile + 2 e (RP = 2 CH); (p, hj, c) advance incrementally (NT = DR CH + DC,
-    // DR = DP PHT + DH: at most one carry each)
+  // (WIDE) walk this thread's 16-byte chunks in linear order: chunk e = tid + m NT is chunk
+  // c = e % CH of row r = e / CH = (plane p, row hj) and lives at tile + 2 e (RP = 2 CH);
+  // (p, hj, c) advance incrementally (NT = DR CH + DC, DR = DP PHT + DH: at most one carry each)
+  // Kernels with a staging transform in 3D walk plane by plane instead (chunk tid of every
+  // plane, 180 of 256 threads): row, column and coarse-tile offsets are then loop invariants of
+  // the unrolled plane loop, as in the 8-byte path -- the linear walk's per-chunk index
+  // arithmetic made those kernels slower (400^3 prolongation sweep 475 vs 435 us).
+  constexpr bool PLANE_WALK = WIDE && LOAD != L_PLAIN && DIM == 3;
+  auto walk_chunks = [&](auto&& f) {
     constexpr int CH = RP / 2, DR = TC::NT / CH, DC = TC::NT % CH, DP = DR / PHT, DH = DR % PHT;
-    static_assert(RP % 2 == 0 && DH + 1 <= PHT, "one carry per step");
+    static_assert(!WIDE || (RP % 2 == 0 && DH + 1 <= PHT), "one carry per step");
+    if constexpr (PLANE_WALK) {
+      constexpr int NCHP = PHT * CH;
+      static_assert(!PLANE_WALK || NCHP <= TC::NT, "one chunk per thread and plane");
+      if (tid < NCHP) {
+        const int hj = tid / CH, c = tid - hj * CH;
+#pragma unroll
+        for (int p = 0; p < TI + 2; ++p)
+          if (p < ni + 2) f(p * NCHP + tid, p, hj, c);
+      }
+      return;
+    }
     const int total = (ni + 2) * PHT * CH;
     int r0 = tid / CH, c = tid - r0 * CH;
     int p = DIM == 3 ? r0 / PHT : r0, hj = DIM == 3 ? r0 - p * PHT : 0;
-    const int jmax = DIM == 3 ? g.n - (j0 - 1) : 0;
-    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(tile));
     for (int e = tid; e < total; e += TC::NT) {
-      const uint32_t lin = lin0 + (uint32_t)p * pstride + (DIM == 3 ? (uint32_t)hj * (uint32_t)g.s : 0u) + 2u * (uint32_t)c;
-      const uint32_t par = (uint32_t)(a00 ^ ((p + hj) & 1));
-      const bool ok = hj <= jmax && lin < tl.vend + par;  // chunk start lin - par inside the vector
-      // (pointer arithmetic, not index arithmetic: lin - par wraps for the first element of a vector
-      // that starts 8 bytes into a 16-byte chunk, e.g. the w half of a stacked [u; w])
-      cp_async16(sbase + (unsigned)e * 16u, ok ? (a.x + lin) - par : (a.x + lin0) - a00, ok);
+      f(e, p, hj, c);
       c += DC;
       int dr = DR;
       if (c >= CH) {
@@ -372,6 +381,18 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
         p += dr;
       }
     }
+  };
+  if constexpr (WIDE) {
+    const int jmax = DIM == 3 ? g.n - (j0 - 1) : 0;
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(tile));
+    walk_chunks([&](int e, int p, int hj, int c) {
+      const uint32_t lin = lin0 + (uint32_t)p * pstride + (DIM == 3 ? (uint32_t)hj * (uint32_t)g.s : 0u) + 2u * (uint32_t)c;
+      const int par = a00 ^ ((p + hj) & 1);
+      const bool ok = hj <= jmax && lin < tl.vend + (uint32_t)par;  // chunk start lin - par inside the vector
+      // (pointer arithmetic, not index arithmetic: lin - par wraps for the first element of a vector
+      // that starts 8 bytes into a 16-byte chunk, e.g. the w half of a stacked [u; w])
+      cp_async16(sbase + (unsigned)e * 16u, ok ? (a.x + lin) - par : (a.x + lin0) - a00, ok);
+    });
   } else if (PLANE_ISSUE) {
 #pragma unroll
     for (int p = 0; p < TI + 2; ++p) {
@@ -418,7 +439,47 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     __syncthreads();  // ... and everyone's: the coarse tile is visible
   }
   cp_wait<0>();
-  if (LOAD != L_PLAIN) {
+  if constexpr (WIDE && LOAD != L_PLAIN) {
+    // staging transform on this thread's own chunks (two elements each, 16-byte shared-memory
+    // accesses), same arithmetic per element as the 8-byte path below
+    if (!fold) {
+      constexpr int CSI = CT::CJ * CT::CK, CSJ = CT::CK;
+      const double wd = a.omega * op.invd;
+      walk_chunks([&](int e, int p, int hj, int c) {
+        double2* q = reinterpret_cast<double2*>(tile) + e;
+        double2 v = *q;
+        const int ip = i0 - 1 + p, gj = DIM == 3 ? j0 - 1 + hj : 0;
+        const int gk = k0 - 1 + 2 * c - (a00 ^ ((p + hj) & 1));  // column of the chunk's first element
+        if (LOAD == L_JAC0) {
+          if (inner) {
+            v.x = wd * v.x;
+            v.y = wd * v.y;
+          } else {
+            const int cij = DIM == 3 ? cdig(ip, g.n) * 9 + cdig(gj, g.n) * 3 : cdig(ip, g.n) * 3;
+            const int c0 = cij + cdig(gk, g.n), c1 = cij + cdig(gk + 1, g.n);
+            const bool rowin = DIM == 2 || gj <= g.n;
+            const double d0 = (c0 == Traits<DIM>::INTERIOR || !rowin || gk < 0 || gk > g.n)
+                                  ? op.invd
+                                  : __ldg(op.tab + c0 * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+            const double d1 = (c1 == Traits<DIM>::INTERIOR || !rowin || gk + 1 > g.n)
+                                  ? op.invd
+                                  : __ldg(op.tab + c1 * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+            v.x = a.omega * d0 * v.x;
+            v.y = a.omega * d1 * v.y;
+          }
+        } else {
+          // e -> e + P e_c from the coarse tile (slots outside the box read junk that is never used)
+          const int pl = ((ip >> 1) - cbi) * CSI + (DIM == 3 ? ((gj >> 1) - cbj) * CSJ : 0) - cbk;
+          const int pu = (((ip + 1) >> 1) - cbi) * CSI + (DIM == 3 ? (((gj + 1) >> 1) - cbj) * CSJ : 0) - cbk;
+          const double t0 = fma(0.5, ct[pu + ((gk + 1) >> 1)], 0.5 * ct[pl + (gk >> 1)]);
+          const double t1 = fma(0.5, ct[pu + ((gk + 2) >> 1)], 0.5 * ct[pl + ((gk + 1) >> 1)]);
+          v.x = v.x + t0;
+          v.y = v.y + t1;
+        }
+        *q = v;
+      });
+    }
+  } else if (LOAD != L_PLAIN) {
     // the transform touches only this thread's own staged elements (the per-plane
     // issue mapping), so no barrier is needed before it; L_PROLONG reads the coarse
     // tile published above, the fallback path (no coarse tile) reads global memory
