@@ -342,6 +342,43 @@ def test_solver_knobs_match_oracle(port_lib, kw, dim, n, mode):
     ctx.close()
 
 
+@pytest.mark.parametrize("dim,n", [(3, 64), (3, 48), (3, 72), (3, 40), (2, 512), (2, 320), (2, 136)])
+def test_wide_staging_bit_identical(monkeypatch, dim, n):
+    """k_tiled's 16-byte staging (rows fetched from their address rounded down to 16 bytes, the
+    row parity folded into the tap addresses) against the 8-byte staging: every tiled operator
+    and a Newton step have the same bits -- on grids whose tiles are cut by the box (40, 48,
+    72, 136, 320), for both halves of a stacked vector (the w half of [u; w] starts 8 bytes into a
+    16-byte chunk when N is odd) and on every tiled level (tiled_min_n=2: thin tiles too)."""
+    cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, gmres_tol=1e-10, gmres_restart=30)
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-1, 1, (n + 1) ** dim)
+    x2 = rng.uniform(-1, 1, 2 * (n + 1) ** dim)
+    u0 = okg.seeded_ic((n + 1) ** dim, 1, 0.0)
+    outs = []
+    for wide, extra in (("0", {}), ("", {}), ("", dict(tiled_min_n=2, mg_fuse=-1, tail_max_vertices=-1))):
+        if wide:
+            monkeypatch.setenv("OKG_WIDE", wide)
+        else:
+            monkeypatch.delenv("OKG_WIDE", raising=False)
+        ctx = okg.SchurContext(cfg, **extra)
+        ctx.linearize(u0)
+        res = [ctx.apply(k, x) for k in (_lib.OP_M, _lib.OP_K, _lib.OP_SHAT, _lib.OP_VCYCLE, _lib.OP_SHAT_INV,
+                                         _lib.OP_CHEB_M, _lib.OP_CHEB_A, _lib.OP_SCHUR_TILDE_INV)]
+        res += [ctx.apply(k, x2) for k in (_lib.OP_BLOCK, _lib.OP_JACOBIAN)]
+        ctx.clear_linearization()
+        st, stats = okg.newton_solve(okg.State(u0, np.zeros_like(u0)), okg.build_mesh(dim, n, False), ctx)
+        res += [st.u, st.w]
+        outs.append((res, stats.gmres_iters))
+        ctx.close()
+    for other in outs[1:2]:  # same kernel choice, only the staging differs: same bits
+        assert other[1] == outs[0][1]
+        for a, b in zip(other[0], outs[0][0]):
+            assert np.array_equal(a, b)
+    # every level tiled (other kernels on the small levels): same iteration counts, fields to rounding
+    assert outs[2][1] == outs[0][1]
+    assert relerr(outs[2][0][-2], outs[0][0][-2]) <= 1e-10
+
+
 @pytest.mark.parametrize("dim,n", [(2, 64), (2, 256), (3, 32), (3, 16), (3, 64)])
 def test_fused_vcycle_bit_identical(dim, n):
     # okg_vcycle.cuh claims the same arithmetic per vertex as the unfused kernels

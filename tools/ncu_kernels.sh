@@ -7,7 +7,7 @@ set -u
 P=${1:-m}
 for spec in "resid 1 0 1" "pre2 2 1 2" "prolong 7 2 2"; do
   set -- $spec
-  RX="k_tiled<.int.3, .int.$3, .int.$4, .int.8>"
+  RX="k_tiled<.int.3, .int.$3, .int.$4, .int.8,"
   KBASE=demangled KREGEX="$RX" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 128 5 $2" bash tools/ncu_full.sh ${P}_${1}128 > /dev/null 2>&1
   OKG_MIN_COARSE=17576 KBASE=demangled KREGEX="$RX" SKIP=3 COUNT=1 CMD="python tools/kbench.py 3 400 5 $2" bash tools/ncu_full.sh ${P}_${1}400 > /dev/null 2>&1
   for f in ${P}_${1}128 ${P}_${1}400; do

@@ -40,8 +40,8 @@ EXTRA = ["l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput
          "smsp__pcsamp_warps_issue_stalled_selected", "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 # kernel tag -> (template, algorithmic bytes per vertex, what they are)
-KERNELS = {"resid": ("k_tiled<3,L_PLAIN,T_RESID,8>", 24.0, "x, b read; r written"),
-           "pre2": ("k_tiled<3,L_JAC0,T_JACOBI,8>", 16.0, "r read; e written (two pre-sweeps from zero)"),
+KERNELS = {"resid": ("k_tiled<3,L_PLAIN,T_RESID,8,WIDE>", 24.0, "x, b read; r written"),
+           "pre2": ("k_tiled<3,L_JAC0,T_JACOBI,8,WIDE>", 16.0, "r read; e written (two pre-sweeps from zero)"),
            "prolong": ("k_tiled<3,L_PROLONG,T_JACOBI,8>", 25.0, "e, b read, e_c read (1/8); e' written")}
 KID = {"resid": 1, "pre2": 2, "prolong": 7}
 traffic = {}
