@@ -364,6 +364,32 @@ static void write_red(okg_ctx* c, int off, int cnt) {
   CK(cudaMemcpyAsync(c->dred + off, c->hred + off, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 }
 
+// The per-slab partial sums a kernel just left in dred[off .. off+cnt), summed over the slabs:
+//  * reduce_to_host: the totals in hred on every slab (the host decides something with them);
+//  * reduce_on_device: the totals in dred for the NEXT KERNEL -- with one process per GPU this
+//    is one in-stream ncclAllReduce on the device scalars and no host round trip at all (the
+//    CGS2 passes of an Arnoldi step chain three of them); the thread transport reduces on the
+//    host in rank order (one stream synchronisation per reduction).
+static void reduce_to_host(okg_ctx* c, int off, int cnt) {
+  if (c->nslabs > 1 && c->comm) {
+    NCK(c, c->ncl->AllReduce(c->dred + off, c->dred + off, cnt, ncclDouble, ncclSum, c->comm, c->stream));
+    sync_read(c, off, cnt);
+    return;
+  }
+  sync_read(c, off, cnt);
+  allreduce(c, off, cnt);
+}
+static void reduce_on_device(okg_ctx* c, int off, int cnt) {
+  if (c->nslabs == 1) return;
+  if (c->comm) {
+    NCK(c, c->ncl->AllReduce(c->dred + off, c->dred + off, cnt, ncclDouble, ncclSum, c->comm, c->stream));
+    return;
+  }
+  sync_read(c, off, cnt);
+  allreduce(c, off, cnt);
+  write_red(c, off, cnt);
+}
+
 static int reg_index(okg_ctx* c, const double* x, int l) {
   for (size_t q = 0; q < c->reg.size(); ++q)
     if (c->reg[q].first == x && c->reg[q].second == l) return (int)q;
@@ -1285,8 +1311,7 @@ static double residual(okg_ctx* c, const double* un, const double* wn, const dou
   launch(c, k_residual<DIM>, own(c->fine), BS, 0, c->fine, dev_op<DIM>(c->M), dev_op<DIM>(c->K), c->nl, a,
                                                    red(c, R_RES));
   note(c);
-  sync_read(c, R_RES, 2);
-  allreduce(c, R_RES, 2);
+  reduce_to_host(c, R_RES, 2);
   const double na = std::sqrt(c->hred[R_RES]), nb = std::sqrt(c->hred[R_RES + 1]);
   if (s1out) *s1out = c->hred[R_RES] + c->hred[R_RES + 1];
   return std::sqrt(na * na + nb * nb);  // stacked_norm, model.hpp:152-155
@@ -1321,27 +1346,15 @@ static void arnoldi_ortho(okg_ctx* c, int nv) {
   launch(c, k_arnoldi_dot<NVB>, vblk(ne), BS, 0, nv, (const double*)pw, (const double*)c->V, n2, c->seg, ne,
          red(c, R_H));
   note(c);
-  if (c->nslabs > 1) {
-    sync_read(c, R_H, NVB + 1);
-    allreduce(c, R_H, NVB + 1);
-    write_red(c, R_H, NVB + 1);
-  }
+  reduce_on_device(c, R_H, NVB + 1);
   launch(c, k_arnoldi_update<NVB, 0>, vblk(ne), BS, 0, nv, (const double*)pw, (const double*)c->V, n2, c->seg, ne,
          (const double*)(c->dred + R_H), gt, red(c, R_C));
   note(c);
-  if (c->nslabs > 1) {
-    sync_read(c, R_C, NVB);
-    allreduce(c, R_C, NVB);
-    write_red(c, R_C, NVB);
-  }
+  reduce_on_device(c, R_C, NVB);
   launch(c, k_arnoldi_update<NVB, 1>, vblk(ne), BS, 0, nv, (const double*)gt, (const double*)c->V, n2, c->seg, ne,
          (const double*)(c->dred + R_C), pw, red(c, R_NRM));
   note(c);
-  if (c->nslabs > 1) {
-    sync_read(c, R_NRM, 1);
-    allreduce(c, R_NRM, 1);
-    write_red(c, R_NRM, 1);
-  }
+  reduce_on_device(c, R_NRM, 1);
 }
 
 // generic (nv > 32): chunked classical Gram-Schmidt twice
@@ -1357,8 +1370,7 @@ static void arnoldi_ortho_chunked(okg_ctx* c, int nv, std::vector<double>& hsum,
       launch(c, k_arnoldi_dot<32>, vblk(ne), BS, 0, cnt, (const double*)pw, (const double*)(c->V + (size_t)q0 * n2),
              n2, c->seg, ne, red(c, R_H));
       note(c);
-      sync_read(c, R_H, 33);
-      allreduce(c, R_H, 33);
+      reduce_to_host(c, R_H, 33);
       for (int q = 0; q < cnt; ++q) hh[q0 + q] = c->hred[R_H + q];
       if (pass == 0 && q0 == 0) ww = c->hred[R_H + 32];
     }
@@ -1374,8 +1386,7 @@ static void arnoldi_ortho_chunked(okg_ctx* c, int nv, std::vector<double>& hsum,
     }
     for (int q = 0; q < nv; ++q) hsum[q] += hh[q];
   }
-  sync_read(c, R_NRM, 1);
-  allreduce(c, R_NRM, 1);
+  reduce_to_host(c, R_NRM, 1);
   write_red(c, R_NRM, 1);
 }
 
@@ -1396,8 +1407,7 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
   if (nb2 < 0.0) {
     launch(c, k_dot, vblk(ne), BS, 0, (const double*)F(c, b), (const double*)F(c, b), c->seg, ne, red(c, R_DOT));
     note(c);
-    sync_read(c, R_DOT, 1);
-    allreduce(c, R_DOT, 1);
+    reduce_to_host(c, R_DOT, 1);
     nb2 = c->hred[R_DOT];
   }
   // require_finite(b) (krylov.hpp:52): any NaN/Inf entry makes the sum of squares non-finite
@@ -1504,8 +1514,7 @@ static int gmres(okg_ctx* c, const double* b, double* x, double rel_tol, int max
     axpy(c, 1.0, F(c, c->pz), F(c, x), n2);
     // r = b - J x, beta = ||r||   (krylov.hpp:135-138)
     capply<DIM, CM_JAC_RES>(c, x, x + c->B, b, c->gr, c->dt_theta, red(c, R_JRES));
-    sync_read(c, R_JRES, 1);
-    allreduce(c, R_JRES, 1);
+    reduce_to_host(c, R_JRES, 1);
     beta = std::sqrt(c->hred[R_JRES]);
     st->final_residual = beta;
     r = c->gr;
@@ -1557,8 +1566,7 @@ static void lanczos_bounds(okg_ctx* c, ApplyB&& apply_B, const char* what, doubl
   auto dot = [&](const double* x, const double* y) {
     launch(c, k_dot, vblk(nloc), BS, 0, (const double*)F(c, x), (const double*)F(c, y), s1, nloc, red(c, R_DOT));
     note(c);
-    sync_read(c, R_DOT, 1);
-    allreduce(c, R_DOT, 1);
+    reduce_to_host(c, R_DOT, 1);
     return c->hred[R_DOT];
   };
   std::vector<double*> Vv;
@@ -1688,8 +1696,7 @@ static double dotv(okg_ctx* c, const double* a, const double* b) {
   const Seg s1{c->seg.off, ne, c->B};
   launch(c, k_dot, vblk(ne), BS, 0, (const double*)F(c, a), (const double*)F(c, b), s1, ne, red(c, R_DOT));
   note(c);
-  sync_read(c, R_DOT, 1);
-  allreduce(c, R_DOT, 1);
+  reduce_to_host(c, R_DOT, 1);
   return c->hred[R_DOT];
 }
 
@@ -1756,8 +1763,7 @@ template <int DIM>
 static double total_mass_impl(okg_ctx* c, const double* u) {
   launch(c, k_mass<DIM>, vblk(c->fine.hi - c->fine.lo), BS, 0, c->fine, (const double*)c->b_tab, u, red(c, R_DOT));
   note(c);
-  sync_read(c, R_DOT, 1);
-  allreduce(c, R_DOT, 1);
+  reduce_to_host(c, R_DOT, 1);
   return c->hred[R_DOT];
 }
 
@@ -1770,8 +1776,7 @@ static double double_well_impl(okg_ctx* c, const double* u) {
   const double vol = DIM == 2 ? c->h * c->h / 2.0 : c->h * c->h * c->h / 6.0;
   launch(c, k_double_well<DIM>, vblk(cells), BS, 0, g, vol, u, red(c, R_DOT));
   note(c);
-  sync_read(c, R_DOT, 1);
-  allreduce(c, R_DOT, 1);
+  reduce_to_host(c, R_DOT, 1);
   return c->hred[R_DOT];
 }
 
