@@ -349,6 +349,11 @@ def main():
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch under torchrun (127.0.0.1 rendezvous)
+        if args.impl != "reference":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs on this node, found {have}")
         import socket
         with socket.socket() as sk:
             sk.bind(("127.0.0.1", 0))
