@@ -44,9 +44,12 @@ KERNELS = {"resid": ("k_tiled<3,L_PLAIN,T_RESID,8,WIDE>", 24.0, "x, b read; r wr
            "pre2": ("k_tiled<3,L_JAC0,T_JACOBI,8,WIDE>", 16.0, "r read; e written (two pre-sweeps from zero)"),
            "prolong": ("k_tiled<3,L_PROLONG,T_JACOBI,8>", 25.0, "e, b read, e_c read (1/8); e' written")}
 KID = {"resid": 1, "pre2": 2, "prolong": 7}
+KERNELS2D = {"cheb": ("k_tiled<2,L_PLAIN,T_CHEB,8>", 48.0, "d, r, x read; d', r', x' written")}
+KID["cheb"] = 4
 traffic = {}
-for n, key, verts in ((128, "c4_3d128", 129 ** 3), (400, "c5_3d800", 401 ** 3)):
-    for tag, (tmpl, bpv, what) in KERNELS.items():
+for dim, n, key, verts in ((3, 128, "c4_3d128", 129 ** 3), (3, 400, "c5_3d800", 401 ** 3),
+                           (2, 2048, "c2_2d2048", 2049 ** 2)):
+    for tag, (tmpl, bpv, what) in (KERNELS if dim == 3 else KERNELS2D).items():
         try:
             rows = list(csv.reader(open(f"{G}/{P}_{tag}{n}_raw.csv")))
         except OSError:
@@ -56,10 +59,10 @@ for n, key, verts in ((128, "c4_3d128", 129 ** 3), (400, "c5_3d800", 401 ** 3)):
         h, units, d = rows[0], rows[1], rows[2]
         ix = {k: i for i, k in enumerate(h)}
         env = "OKG_MIN_COARSE=17576 " if n == 400 else ""
-        out = [f"# ncu --set full --clock-control none (cold caches), fine-level {tmpl}, 3D {n}^3 "
+        out = [f"# ncu --set full --clock-control none (cold caches), fine-level {tmpl}, {dim}D {n}^{dim} "
                f"({P} run of tools/measure_round.sh)",
-               f"# command: {env}KBASE=demangled KREGEX='k_tiled<3,...>' SKIP=3 COUNT=1 "
-               f"CMD='python tools/kbench.py 3 {n} 5 {KID[tag]}' bash tools/ncu_full.sh",
+               f"# command: {env}KBASE=demangled KREGEX='k_tiled<DIM,LOAD,EPI,8,' SKIP=3 COUNT=1 "
+               f"CMD='python tools/kbench.py {dim} {n} 5 {KID[tag]}' bash tools/ncu_full.sh",
                f"{'Kernel Name':70s} {d[ix['Kernel Name']]}"]
         out += [f"{m:70s} {d[ix[m]]} {units[ix[m]]}" for m in METRICS + EXTRA if m in ix]
         out.append(f"# algorithmic bytes per launch: {bpv:g} B x {verts} vertices = {bpv * verts / 1e6:.1f} MB ({what})")
