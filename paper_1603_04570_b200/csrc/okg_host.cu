@@ -1125,6 +1125,10 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
   // and is gone: DESIGN section 5)
   for (int j = 0; j + 1 < k; ++j) {
     const int last = (j == k - 2);
+    // x is updated every other step from j = 1 on: an odd step with a successor leaves x alone
+    // (mode 1), the even step after it adds both directions in the reference's order (mode 2,
+    // bit-identical): 16 of 48 B/vertex less on the skipped steps of an HBM-bound kernel
+    const int xmode = j == 0 ? 0 : ((j & 1) ? (last ? 0 : 1) : 2);
     exchange(c, 0, dcur);
     if (c->lv[0].tiled) {
       TArgs a = targs(dcur, j == 0 ? b : c->cr, c->cr, x, 0.0);
@@ -1133,10 +1137,11 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
       a.c1 = c->cheb_c1[j];
       a.c2 = c->cheb_c2[j];
       a.last = last;
+      a.xmode = xmode;
       tiled<DIM, L_PLAIN, T_CHEB>(c, c->lv[0], A, a);
     } else {
       launch(c, k_cheb_step<DIM>, own(g), BS, 0, g, o, dcur, j == 0 ? b : c->cr, j == 0 ? dcur : x, dnxt,
-                                                        c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last);
+                                                        c->cr, x, c->cheb_c1[j], c->cheb_c2[j], last, xmode);
       note(c);
     }
     std::swap(dcur, dnxt);
@@ -3167,7 +3172,7 @@ static void kernel_timing_impl(okg_ctx* c, int which, int reps, int flags, doubl
           tiled<DIM, L_PLAIN, T_CHEB>(c, L0, c->A, a);
         } else {
           launch(c, k_cheb_step<DIM>, own(g), BS, 0, g, dev_op<DIM>(c->A), x, b, y, c->zz, c->rr, z,
-                                                            c->cheb_c1[0], c->cheb_c2[0], 0);
+                                                            c->cheb_c1[0], c->cheb_c2[0], 0, 0);
           note(c);
         }
         break;

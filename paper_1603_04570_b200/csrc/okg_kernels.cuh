@@ -469,7 +469,7 @@ template <int DIM>
 __global__ void __launch_bounds__(BS) k_cheb_step(Grid g, Op<DIM> A, const double* __restrict__ d,
                                                   const double* r_in, const double* x_in,
                                                   double* __restrict__ d_out, double* r_out, double* x_out,
-                                                  double c1, double c2, int last) {
+                                                  double c1, double c2, int last, int xmode) {
   PDL_ENTRY();
   const uint32_t idx = g.lo + blockIdx.x * BS + threadIdx.x;
   if (idx >= g.hi) return;
@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(BS) k_cheb_step(Grid g, Op<DIM> A, const doubl
   const double r = r_in[idx] - ad;
   const double z = r * op_invd<DIM>(A, nd.cls);
   const double dn = fma(c1, d[idx], c2 * z);
-  x_out[idx] = x_in[idx] + dn;
+  // (xmode: see TArgs / epilogue_pre<T_CHEB>)
+  if (xmode != 1) x_out[idx] = (xmode == 2 ? x_in[idx] + d[idx] : x_in[idx]) + dn;
   if (!last) {
     d_out[idx] = dn;
     r_out[idx] = r;

@@ -95,6 +95,7 @@ struct TArgs {
   double* y2;        // d_out (cheb)
   double omega, c1, c2;
   int32_t last;
+  int32_t xmode;     // T_CHEB: 0: x' = x + d'; 1: x untouched this step; 2: x' = (x + d) + d' (the step before was 1)
   Grid gc;           // coarse grid (L_PROLONG)
 };
 
@@ -166,7 +167,10 @@ __device__ __forceinline__ void epilogue_pre(const TArgs& a, uint32_t idx, doubl
     const double r = bv - As;
     const double z = r * invd;
     const double dn = fma(a.c1, s_own, a.c2 * z);
-    a.acc[idx] = pv + dn;
+    // x_{k+1} = x_k + d_{k+1} (krylov.hpp:196); every other step leaves x alone and the next one
+    // adds both directions in the reference's order, (x + d_k) + d_{k+1} -- d_k is this step's
+    // staged operand -- the same bits for 16 B/vertex less on the skipped step
+    if (a.xmode != 1) a.acc[idx] = (a.xmode == 2 ? pv + s_own : pv) + dn;
     if (!a.last) {
       a.y2[idx] = dn;
       a.y[idx] = r;
@@ -230,7 +234,7 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
     for (int o = 0; o < NO; ++o) As = fma(wv[o], sv[o], As);
   }
   const double bv = EpiNeeds<EPI>::B ? a.b[idx] : 0.0;
-  const double pv = EPI == T_CHEB ? a.x2[idx] : (EPI == T_JACOBI_ACC ? a.acc[idx] : 0.0);
+  const double pv = EPI == T_CHEB ? (a.xmode == 1 ? 0.0 : a.x2[idx]) : (EPI == T_JACOBI_ACC ? a.acc[idx] : 0.0);
   epilogue_pre<DIM, EPI>(a, idx, s_own, As, __ldg(w + NO), bv, pv);
 }
 
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     const bool ok = active && t < ni;
     const uint32_t idx = idx0 + (uint32_t)t * pstride;
     pb[t] = (EpiNeeds<EPI>::B && ok && !fold) ? a.b[idx] : 0.0;
-    pp[t] = (EpiNeeds<EPI>::P2 && ok) ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx]) : 0.0;
+    pp[t] = (EpiNeeds<EPI>::P2 && ok && !(EPI == T_CHEB && a.xmode == 1)) ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx]) : 0.0;
   }
   // L_PROLONG: coarse tile covering the fine planes/rows/columns of the staged tile
   using CT = CoarseTile<DIM, TI>;
