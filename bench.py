@@ -531,6 +531,10 @@ def main():
                         "avg_launch_us": d["instep_us"],
                         "share_of_step": d["share_of_step"], "cold_us": d["cold_us"],
                         "cold_frac": d["cold_gbs"] / peak}
+            if roofline["frac"] > 1.0:
+                roofline["note"] = ("in-step time above the measured copy peak: part of this kernel's operands "
+                                    "(written by the previous kernels of the step) is still in the 126 MB L2; "
+                                    "cold_frac is the HBM-only figure")
             prof = os.path.join(ROOT, "profiles", "traffic.json")
             if os.path.exists(prof):
                 try:
