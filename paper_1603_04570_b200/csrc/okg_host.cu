@@ -125,6 +125,7 @@ struct okg_ctx {
   double lambda_lo = 0, lambda_hi = 0;
   std::vector<double> cheb_c1, cheb_c2;
   double cheb_inv_theta = 0;
+  bool cheb_fuse0 = true;  // first Chebyshev step forms the start vector itself (k_tiled L_CHEB0)
   Grid fine;
   HostOp M, K, A;
   std::vector<Level> lv;
@@ -1115,8 +1116,14 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
   const int k = c->p.cheby_iters;
   double* dcur = c->cd0;
   double* dnxt = c->cd1;
-  launch(c, k_cheb_first<DIM>, own(g), BS, 0, g, o, b, dcur, c->cheb_inv_theta);
-  note(c);
+  // one slab, tiled finest level: the start vector d0 = (D^-1 r)/theta is formed by the first
+  // step's staging transform (k_tiled L_CHEB0, k_cheb_first's rounding): one launch and
+  // 32 B/vertex less per Chebyshev solve.  OKG_CHEB0=0 at okg_create keeps the separate kernel.
+  const bool fuse0 = k >= 2 && c->lv[0].tiled && c->nslabs == 1 && c->cheb_fuse0;
+  if (!fuse0) {
+    launch(c, k_cheb_first<DIM>, own(g), BS, 0, g, o, b, dcur, c->cheb_inv_theta);
+    note(c);
+  }
   if (k == 1) {
     copy(c, dcur + g.lo, x + g.lo, g.hi - g.lo);
     return;
@@ -1129,6 +1136,17 @@ static void cheb(okg_ctx* c, const HostOp& A, const double* b, double* x) {
     // (mode 1), the even step after it adds both directions in the reference's order (mode 2,
     // bit-identical): 16 of 48 B/vertex less on the skipped steps of an HBM-bound kernel
     const int xmode = j == 0 ? 0 : ((j & 1) ? (last ? 0 : 1) : 2);
+    if (j == 0 && fuse0) {
+      TArgs a = targs(b, b, c->cr, x, 0.0);
+      a.y2 = dnxt;
+      a.c1 = c->cheb_c1[0];
+      a.c2 = c->cheb_c2[0];
+      a.inv_theta = c->cheb_inv_theta;
+      a.last = last;
+      tiled<DIM, L_CHEB0, T_CHEB>(c, c->lv[0], A, a);
+      std::swap(dcur, dnxt);
+      continue;
+    }
     exchange(c, 0, dcur);
     if (c->lv[0].tiled) {
       TArgs a = targs(dcur, j == 0 ? b : c->cr, c->cr, x, 0.0);
@@ -2085,6 +2103,7 @@ static void build(okg_ctx* c) {
     if (lmax < lmin) THROW(OKG_EINVAL, "chebyshev: bounds out of order");
     const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
     c->cheb_inv_theta = 1.0 / theta;
+    if (const char* e = std::getenv("OKG_CHEB0")) c->cheb_fuse0 = std::atoi(e) != 0;
     c->cheb_c1.assign(std::max(p.cheby_iters, 1), 0.0);
     c->cheb_c2.assign(std::max(p.cheby_iters, 1), 1.0 / theta);
     if (delta > 1e-300) {

@@ -20,6 +20,8 @@
 //   L_PROLONG stages e + P e_c      -> coarse-grid correction fused into the
 //                                      first post-smoothing sweep
 //                                      (multigrid.hpp:111-115)
+//   L_CHEB0  stages d0 = (D^-1 r)/theta -> the Chebyshev start vector fused into
+//                                      the first Chebyshev step (krylov.hpp:178-182)
 // In 2D the "plane" is a row segment of TK vertices.
 #pragma once
 #include "okg_common.cuh"
@@ -52,7 +54,7 @@ struct Tiling {
   const uint32_t* __restrict__ bnd;  // boundary vertex indices
 };
 
-enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2 };
+enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #ifndef OKG_PROLONG_NOSEL  // coarse-tile P e_c without the all-even select (k_tiled)
 #define OKG_PROLONG_NOSEL 1
 #endif
@@ -94,6 +96,7 @@ struct TArgs {
   const double* x2;  // x_in (cheb) / e_c (prolong)
   double* y2;        // d_out (cheb)
   double omega, c1, c2;
+  double inv_theta;  // L_CHEB0: 1 / theta of the Chebyshev start vector
   int32_t last;
   int32_t xmode;     // T_CHEB: 0: x' = x + d'; 1: x untouched this step; 2: x' = (x + d) + d' (the step before was 1)
   Grid gc;           // coarse grid (L_PROLONG)
@@ -143,6 +146,12 @@ __device__ __forceinline__ double stage_val(const Grid& g, const Op<DIM>& op, co
     const double invd =
         cls == Traits<DIM>::INTERIOR ? op.invd : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
     return a.omega * invd * __ldg(a.x + v);
+  }
+  if (LOAD == L_CHEB0) {  // d0 = (r D^-1) / theta, k_cheb_first's rounding
+    const int cls = class_of<DIM>(g, i, j, k);
+    const double invd =
+        cls == Traits<DIM>::INTERIOR ? op.invd : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+    return (__ldg(a.x + v) * invd) * a.inv_theta;
   }
   // L_PROLONG: e + P e_c  (x + t, t rounded first: multigrid.hpp:111-112)
   const double t = prolong_at<DIM>(a.gc, a.x2, i, j, k);
@@ -234,7 +243,9 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
     for (int o = 0; o < NO; ++o) As = fma(wv[o], sv[o], As);
   }
   const double bv = EpiNeeds<EPI>::B ? a.b[idx] : 0.0;
-  const double pv = EPI == T_CHEB ? (a.xmode == 1 ? 0.0 : a.x2[idx]) : (EPI == T_JACOBI_ACC ? a.acc[idx] : 0.0);
+  const double pv = LOAD == L_CHEB0 ? s_own
+                    : EPI == T_CHEB ? (a.xmode == 1 ? 0.0 : a.x2[idx])
+                                    : (EPI == T_JACOBI_ACC ? a.acc[idx] : 0.0);
   epilogue_pre<DIM, EPI>(a, idx, s_own, As, __ldg(w + NO), bv, pv);
 }
 
@@ -256,6 +267,8 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   pdl_wait();  // (the dependent grid is released below, once the tile is staged)
   using TC = TileCfg<DIM>;
   static_assert(!(WIDE && LOAD == L_PROLONG && TI < 4), "16-byte staging of the prolongation needs the coarse tile");
+  static_assert(!(WIDE && LOAD == L_CHEB0), "the Chebyshev steps keep the 8-byte staging");
+  static_assert(LOAD != L_CHEB0 || EPI == T_CHEB, "L_CHEB0 is the first Chebyshev step");
   constexpr int NO = Traits<DIM>::NOFF;
   constexpr int PHT = TC::PSZ / TC::PW;             // rows per staged plane (1 in 2D)
   constexpr int RP = WIDE ? TC::PW + 2 : TC::PW;    // shared-memory row pitch
@@ -291,7 +304,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   // epilogue's b (a.x == a.b): no transform pass and no prefetch of b
   const bool inner = i0 - 1 >= 1 && i0 + ni <= g.n - 1 && k0 - 1 >= 1 && k0 + TC::TK <= g.n - 1 &&
                      (DIM == 2 || (j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1));
-  const bool fold = OKG_JAC0_FOLD && LOAD == L_JAC0 && inner && a.x == a.b;
+  // (L_CHEB0 the same way: d0 = (r D^-1)/theta with the constant D^-1 of an inner tile is two
+  // multiplies per tap; the raw tile value is the step's r_in, the scaled one its x_in)
+  const bool fold = OKG_JAC0_FOLD && (LOAD == L_JAC0 || LOAD == L_CHEB0) && inner && a.x == a.b;
   // prefetch the pointwise operands of this thread's TI vertices
   double pb[TI], pp[TI];
 #pragma unroll
@@ -299,7 +314,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     const bool ok = active && t < ni;
     const uint32_t idx = idx0 + (uint32_t)t * pstride;
     pb[t] = (EpiNeeds<EPI>::B && ok && !fold) ? a.b[idx] : 0.0;
-    pp[t] = (EpiNeeds<EPI>::P2 && ok && !(EPI == T_CHEB && a.xmode == 1)) ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx]) : 0.0;
+    pp[t] = (EpiNeeds<EPI>::P2 && ok && LOAD != L_CHEB0 && !(EPI == T_CHEB && a.xmode == 1))
+                ? (EPI == T_CHEB ? a.x2[idx] : a.acc[idx])
+                : 0.0;
   }
   // L_PROLONG: coarse tile covering the fine planes/rows/columns of the staged tile
   using CT = CoarseTile<DIM, TI>;
@@ -493,7 +510,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     const double wd = a.omega * op.invd;
     if (fold) {
       // (scale applied in the taps below)
-    } else if (LOAD == L_JAC0 && inner) {
+    } else if ((LOAD == L_JAC0 || LOAD == L_CHEB0) && inner) {
       // branch-free: every slot of this thread (out-of-box / unused slots are never read)
 #pragma unroll
       for (int p = 0; p < TI + 2; ++p)
@@ -501,7 +518,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
         for (int q = 0; q < PER; ++q)
           if (q + 1 < PER || tid + q * TC::NT < TC::PSZ) {
             double& v = tile[p * TC::PSZ + tid + q * TC::NT];
-            v = wd * v;
+            v = LOAD == L_CHEB0 ? (v * op.invd) * a.inv_theta : wd * v;
           }
     } else if (CSTAGE) {
       // coarse-tile offsets of this thread's slots, in-plane part (the plane part per p)
@@ -554,6 +571,12 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
                                     ? op.invd
                                     : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
             v = a.omega * invd * v;
+          } else if (LOAD == L_CHEB0) {
+            const int cls = cip + qcjk[q];
+            const double invd = cls == Traits<DIM>::INTERIOR
+                                    ? op.invd
+                                    : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
+            v = (v * invd) * a.inv_theta;
           } else {
             v = v + prolong_at<DIM>(a.gc, a.x2, ip, qgj[q], qgk[q]);
           }
@@ -584,7 +607,9 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
       const int dk = off_comp(DIM, o, DIM - 1);
       const double raw = (((t + di + dj) & 1) ? tO : tE)[(t + 1 + di) * PSZ + (DIM == 3 ? dj * RP : 0) + dk];
-      const double sv = (OKG_JAC0_FOLD && LOAD == L_JAC0) ? scl * raw : raw;
+      const double sv = (OKG_JAC0_FOLD && LOAD == L_JAC0) ? scl * raw
+                        : (LOAD == L_CHEB0 && fold)       ? (raw * op.invd) * a.inv_theta
+                                                           : raw;
       if (o == Traits<DIM>::CENTER) {
         s_own = sv;
         raw_own = raw;
@@ -592,7 +617,8 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
       As = fma(op.w[o], sv, As);
     }
     if (t < ni)
-      epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, fold ? raw_own : pb[t], pp[t]);
+      epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, fold ? raw_own : pb[t],
+                             LOAD == L_CHEB0 ? s_own : pp[t]);
   }
 }
 
