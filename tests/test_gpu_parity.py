@@ -316,6 +316,30 @@ def test_gmres_long_basis_chunked(port_lib):
     ctx.close()
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 9, 10])
+@pytest.mark.parametrize("dim,n,mode", [(2, 32, "tiled"), (3, 8, "tiled"), (2, 32, "plain"), (3, 32, "default")])
+def test_chebyshev_iteration_counts(monkeypatch, port_lib, k, dim, n, mode):
+    """chebyshev_semi_iteration (krylov.hpp:158-202) for every parity of the iteration count: the
+    tiled path updates x every other step ((x + d_k) + d_{k+1}) and forms the start vector in the
+    first step's staging transform (L_CHEB0) -- both must keep the oracle's values, and the fused
+    start vector the bits of the separate kernel."""
+    modes = dict(MODES, plain=dict(tiled_min_n=-1, mg_fuse=-1))
+    p = po.baseline_params(dim, n, kind="port", cheby_iters=k)
+    o = po.Oracle(p, "port")
+    cfg = okg.SolverConfig(dim=dim, n=n, m=0.0, dt=4e-4, cheby_iters=k)
+    x = np.random.default_rng(10 * k + n).uniform(-1, 1, (n + 1) ** dim)
+    outs = []
+    for fuse0 in ("1", "0"):
+        monkeypatch.setenv("OKG_CHEB0", fuse0)
+        ctx = okg.SchurContext(cfg, **modes[mode])
+        outs.append([ctx.apply(kind, x) for kind in (_lib.OP_CHEB_M, _lib.OP_CHEB_A)])
+        ctx.close()
+    for kind, y in zip((po.CHEB_M, po.CHEB_A), outs[0]):
+        assert relerr(y, o.apply(kind, x)) <= OP_TOL
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
 KNOBS = [dict(cheby_iters=1, mg_cycles=1, richardson_steps=1), dict(mg_pre=1, mg_post=0),
          dict(mg_pre=3, mg_post=1), dict(mg_pre=0, mg_post=2), dict(mg_omega=0.8, richardson_steps=3),
          dict(cheby_iters=4, mg_cycles=2)]
