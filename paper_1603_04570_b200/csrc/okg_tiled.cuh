@@ -58,6 +58,11 @@ enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #ifndef OKG_PROLONG_NOSEL  // coarse-tile P e_c without the all-even select (k_tiled)
 #define OKG_PROLONG_NOSEL 1
 #endif
+#ifndef OKG_WIDE_CA  // 16-byte staging through L1 (.ca) instead of L2 only (.cg).  Measured (A/B on one
+                     // box): .ca is slower -- residual sweep 11.35 vs 10.68 us at 128^3, 289 vs 270 us at
+                     // 400^3, steps 43.6 vs 42.8 ms (128^3), 52.3 vs 51.3 ms (2D); the tiles are read once
+#define OKG_WIDE_CA 0
+#endif
 #ifndef OKG_JAC0_FOLD  // inner JAC0 tiles: scale folded into the taps (see k_tiled)
 #define OKG_JAC0_FOLD 1
 #endif
@@ -109,7 +114,11 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
 }
 // 16-byte cp.async (LDGSTS.128) to a shared-window address, zero-filled when !valid
 __device__ __forceinline__ void cp_async16(unsigned sdst, const double* gmem, bool valid) {
+#if OKG_WIDE_CA
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sdst), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
