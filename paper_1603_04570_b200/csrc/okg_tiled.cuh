@@ -208,11 +208,14 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
                                                 uint32_t t) {
   constexpr int NO = Traits<DIM>::NOFF;
   if (t >= tl.nbnd) return;
+  // everything up to the class weights is static data (written at setup): it is read BEFORE
+  // the grid dependency is waited for, in the shadow of the predecessor's completion
   const uint32_t idx = __ldg(tl.bnd + t);
   const Node<DIM> nd = locate<DIM>(g, idx);
   const double* w = op.tab + nd.cls * (NO + 1);
   double As = 0.0, s_own = 0.0;
   if constexpr (LOAD == L_PROLONG) {
+    pdl_wait();
     // per-slot loop (each staged value needs the coarse correction; the batched
     // form below costs this kernel 16+ registers and a CTA per SM)
 #pragma unroll
@@ -232,6 +235,7 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
     double wv[NO], sv[NO];
 #pragma unroll
     for (int o = 0; o < NO; ++o) wv[o] = __ldg(w + o);
+    pdl_wait();
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
       int ni = nd.i + off_comp(DIM, o, 0);
@@ -273,7 +277,8 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
 // copies, half their shared-memory wavefronts, bit-identical results.
 template <int DIM, int LOAD, int EPI, int TI, int WIDE = 0>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
-  pdl_wait();  // (the dependent grid is released below, once the tile is staged)
+  // (griddepcontrol.wait comes after the index arithmetic and the static loads, right before the
+  // first access to data the predecessor wrote; the dependent grid is released once the tile is staged)
   using TC = TileCfg<DIM>;
   static_assert(!(WIDE && LOAD == L_PROLONG && TI < 4), "16-byte staging of the prolongation needs the coarse tile");
   static_assert(!(WIDE && LOAD == L_CHEB0), "the Chebyshev steps keep the 8-byte staging");
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   // (L_CHEB0 the same way: d0 = (r D^-1)/theta with the constant D^-1 of an inner tile is two
   // multiplies per tap; the raw tile value is the step's r_in, the scaled one its x_in)
   const bool fold = OKG_JAC0_FOLD && (LOAD == L_JAC0 || LOAD == L_CHEB0) && inner && a.x == a.b;
+  pdl_wait();
   // prefetch the pointwise operands of this thread's TI vertices
   double pb[TI], pp[TI];
 #pragma unroll
