@@ -204,10 +204,11 @@ __global__ void __launch_bounds__(BS) k_pre2(Grid g, Op<DIM> op, const double* _
 template <int DIM>
 __global__ void __launch_bounds__(BS) k_restrict(Grid gf, Grid gc, const double* __restrict__ rf,
                                                  double* __restrict__ rc) {
-  PDL_ENTRY();
+  PDL_EARLY();
   const uint32_t idx = gc.lo + blockIdx.x * BS + threadIdx.x;
   if (idx >= gc.hi) return;
   const Node<DIM> nc = locate<DIM>(gc, idx);
+  pdl_wait();  // (index arithmetic first, in the shadow of the predecessor's completion)
   const uint32_t F = (DIM == 3) ? (uint32_t)(2 * nc.i) * gf.ps + (uint32_t)(2 * nc.j) * gf.s + 2 * nc.k
                                 : (uint32_t)(2 * nc.i) * gf.s + 2 * nc.j;
   constexpr int NO = Traits<DIM>::NOFF;
@@ -340,15 +341,18 @@ __device__ __forceinline__ void coarse_sym_block(int nc, const double* __restric
   __shared__ double xs_i[CB], xs_j[CB];
   __shared__ double cpart[8][CB];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // the operator block is static (written at setup): its loads are issued before the grid
+  // dependency is waited for, only x depends on the predecessor
+  const double2* blk = reinterpret_cast<const double2*>(Ap + (size_t)blockIdx.x * CB * CB);
+  double2 a[CB / 8];
+#pragma unroll
+  for (int q = 0; q < CB / 8; ++q) a[q] = __ldcs(blk + (size_t)(w + 8 * q) * (CB / 2) + lane);
+  pdl_wait();
   if (tid < CB) {
     const int r = I * CB + tid, c = J * CB + tid;
     xs_i[tid] = r < nc ? x[r] : 0.0;
     xs_j[tid] = c < nc ? x[c] : 0.0;
   }
-  const double2* blk = reinterpret_cast<const double2*>(Ap + (size_t)blockIdx.x * CB * CB);
-  double2 a[CB / 8];
-#pragma unroll
-  for (int q = 0; q < CB / 8; ++q) a[q] = __ldcs(blk + (size_t)(w + 8 * q) * (CB / 2) + lane);
   __syncthreads();
   const double xj0 = xs_j[2 * lane], xj1 = xs_j[2 * lane + 1];
   double c0 = 0.0, c1 = 0.0;
@@ -378,10 +382,10 @@ __device__ __forceinline__ void coarse_sym_block(int nc, const double* __restric
 __global__ void __launch_bounds__(256) k_coarse_sym(int nc, const double* __restrict__ Ap,
                                                     const double* __restrict__ x, double* __restrict__ R,
                                                     double* __restrict__ Cp) {
-  PDL_ENTRY();
+  PDL_EARLY();
   int I, J;
   tri_index(blockIdx.x, I, J);
-  coarse_sym_block(nc, Ap, x, R, Cp, I, J);
+  coarse_sym_block(nc, Ap, x, R, Cp, I, J);  // (waits for the grid dependency inside)
 }
 
 // y_r (r in block I) = sum_{J <= I} R(I,J)_r + sum_{K > I} C(K,I)_r.  The nb terms
@@ -423,6 +427,7 @@ __device__ __forceinline__ void coarse_sym_rows(int nc, int nb, const double* __
 
 __global__ void __launch_bounds__(CB * CSEG) k_coarse_sym_sum(int nc, int nb, const double* __restrict__ R,
                                                               const double* __restrict__ Cp, double* __restrict__ y) {
+  PDL_EARLY();
   PDL_ENTRY();
   coarse_sym_rows(nc, nb, R, Cp, y, blockIdx.x);
 }

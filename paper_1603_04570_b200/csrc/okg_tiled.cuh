@@ -279,6 +279,8 @@ template <int DIM, int LOAD, int EPI, int TI, int WIDE = 0>
 __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(Grid g, Op<DIM> op, Tiling tl, TArgs a) {
   // (griddepcontrol.wait comes after the index arithmetic and the static loads, right before the
   // first access to data the predecessor wrote; the dependent grid is released once the tile is staged)
+  // (releasing the dependents of a one-wave grid already at entry measured slower: 128^3 step
+  // 44.1 ms for grids <= 592 CTAs, 43.2 ms for <= 296, against 42.4 ms)
   using TC = TileCfg<DIM>;
   static_assert(!(WIDE && LOAD == L_PROLONG && TI < 4), "16-byte staging of the prolongation needs the coarse tile");
   static_assert(!(WIDE && LOAD == L_CHEB0), "the Chebyshev steps keep the 8-byte staging");

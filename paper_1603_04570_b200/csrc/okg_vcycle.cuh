@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_down(Grid g, Grid gc,
   double* W = se2 + RE::SIZE;  // class table
   const int tid = threadIdx.x;
   constexpr int U = 8;
+  PDL_EARLY();
   load_table<DIM, B::NT>(W, op);
   PDL_ENTRY();
   table_wait();
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(MgBox<DIM, BX>::NT) k_mg_up(Grid g, Grid gc, O
   double* W = sbq + RQ::SIZE;  // class table
   const int tid = threadIdx.x;
   constexpr int U = 8;
+  PDL_EARLY();
   load_table<DIM, B::NT>(W, op);
   PDL_ENTRY();
   for (int base = tid; base < RP::SIZE; base += B::NT * U) {
