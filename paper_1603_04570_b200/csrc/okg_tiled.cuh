@@ -24,6 +24,8 @@
 //                                      the first Chebyshev step (krylov.hpp:178-182)
 // In 2D the "plane" is a row segment of TK vertices.
 #pragma once
+#include <type_traits>
+
 #include "okg_common.cuh"
 
 namespace okg {
@@ -65,6 +67,9 @@ enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #endif
 #ifndef OKG_JAC0_FOLD  // inner JAC0 tiles: scale folded into the taps (see k_tiled)
 #define OKG_JAC0_FOLD 1
+#endif
+#ifndef OKG_FOLD_FACES  // ... and tiles that touch the boundary along one axis only
+#define OKG_FOLD_FACES 1
 #endif
 enum TEpi {
   T_APPLY = 0,       // y = A s
@@ -322,7 +327,35 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
                      (DIM == 2 || (j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1));
   // (L_CHEB0 the same way: d0 = (r D^-1)/theta with the constant D^-1 of an inner tile is two
   // multiplies per tap; the raw tile value is the step's r_in, the scaled one its x_in)
-  const bool fold = OKG_JAC0_FOLD && (LOAD == L_JAC0 || LOAD == L_CHEB0) && inner && a.x == a.b;
+  // A tile that touches the boundary along ONE axis only folds as well (OKG_FOLD_FACES): the boundary
+  // vertices in its halo are then all of one face class per side, reached only by the taps whose offset
+  // component along that axis points at the face -- those taps take the face class' scale from a
+  // register (s_m / s_p; a compile-time choice per tap in the sweep specialised for the axis), every
+  // other tap the interior one.  Same products, same bits; at 128^3 this folds 88 % of the core tiles
+  // instead of 38 %, and all levels below get folded tiles at all (64^3: 0 -> 68 %).
+  const bool fi = !(i0 - 1 >= 1 && i0 + ni <= g.n - 1);
+  const bool fk = !(k0 - 1 >= 1 && k0 + TC::TK <= g.n - 1);
+  const bool fj = DIM == 3 && !(j0 - 1 >= 1 && j0 + TC::TJ <= g.n - 1);
+  const int fax = OKG_FOLD_FACES ? ((int)fi + (int)fj + (int)fk <= 1 ? (fi ? 1 : fj ? 2 : fk ? 3 : 0) : -1)
+                                 : (inner ? 0 : -1);
+  const bool fold = OKG_JAC0_FOLD && (LOAD == L_JAC0 || LOAD == L_CHEB0) && fax >= 0 && a.x == a.b;
+  // tap scales of a folded tile (1.0 -- exact -- on a JAC0 tile that is not folded); static data
+  double sc0 = 1.0, s_m = 1.0, s_p = 1.0;
+  if constexpr (LOAD == L_JAC0 || LOAD == L_CHEB0) {
+    if (fold) {
+      sc0 = LOAD == L_JAC0 ? a.omega * op.invd : op.invd;
+      s_m = s_p = sc0;
+      if (fax > 0) {
+        const int st = DIM == 3 ? (fax == 1 ? 9 : fax == 2 ? 3 : 1) : (fax == 1 ? 3 : 1);  // class digit stride
+        const bool lo = fax == 1 ? i0 - 1 == 0 : fax == 2 ? j - 1 == 0 : k - 1 == 0;
+        const bool hi = fax == 1 ? i0 + ni == g.n : fax == 2 ? j + 1 == g.n : k + 1 == g.n;
+        const double dl = __ldg(op.tab + (Traits<DIM>::INTERIOR - st) * (NO + 1) + NO);
+        const double dh = __ldg(op.tab + (Traits<DIM>::INTERIOR + st) * (NO + 1) + NO);
+        if (lo) s_m = LOAD == L_JAC0 ? a.omega * dl : dl;
+        if (hi) s_p = LOAD == L_JAC0 ? a.omega * dh : dh;
+      }
+    }
+  }
   pdl_wait();
   // prefetch the pointwise operands of this thread's TI vertices
   double pb[TI], pp[TI];
@@ -608,34 +641,47 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   if (!active) return;
   // all TI vertex chains are computed unconditionally (no branch between them, so
   // their dependent FMA chains interleave); only the stores are predicated
-  // JAC0: taps scaled by scl (wd on folded tiles, else 1.0 -- exact)
-  const double scl = fold ? a.omega * op.invd : 1.0;
   // this thread's centre column in rows whose (plane + row) parity equals / differs from its
   // own row's: one pointer without WIDE, two (shifted by the rows' address parity) with it
   const int q0 = DIM == 3 ? (tj & 1) : 1;
   const double* tE = tile + (DIM == 3 ? (tj + 1) * RP : 0) + tk + 1 + (WIDE ? (a00 ^ q0) : 0);
   const double* tO = tile + (DIM == 3 ? (tj + 1) * RP : 0) + tk + 1 + (WIDE ? (a00 ^ q0 ^ 1) : 0);
+  // AX: the axis along which a folded tile touches the boundary (0 none, 1 x, 2 y, 3 fastest)
+  auto sweep = [&](auto AXC) {
+    constexpr int AX = decltype(AXC)::value;
 #pragma unroll
-  for (int t = 0; t < TI; ++t) {
-    double As = 0.0, s_own = 0.0, raw_own = 0.0;
+    for (int t = 0; t < TI; ++t) {
+      double As = 0.0, s_own = 0.0, raw_own = 0.0;
+      const double sp_t = (AX == 1 && t == ni - 1) ? s_p : sc0;  // x face above: the tile's last plane only
 #pragma unroll
-    for (int o = 0; o < NO; ++o) {
-      const int di = off_comp(DIM, o, 0);
-      const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
-      const int dk = off_comp(DIM, o, DIM - 1);
-      const double raw = (((t + di + dj) & 1) ? tO : tE)[(t + 1 + di) * PSZ + (DIM == 3 ? dj * RP : 0) + dk];
-      const double sv = (OKG_JAC0_FOLD && LOAD == L_JAC0) ? scl * raw
-                        : (LOAD == L_CHEB0 && fold)       ? (raw * op.invd) * a.inv_theta
-                                                           : raw;
-      if (o == Traits<DIM>::CENTER) {
-        s_own = sv;
-        raw_own = raw;
+      for (int o = 0; o < NO; ++o) {
+        const int di = off_comp(DIM, o, 0);
+        const int dj = DIM == 3 ? off_comp(DIM, o, 1) : 0;
+        const int dk = off_comp(DIM, o, DIM - 1);
+        const double raw = (((t + di + dj) & 1) ? tO : tE)[(t + 1 + di) * PSZ + (DIM == 3 ? dj * RP : 0) + dk];
+        const int da = AX == 1 ? di : AX == 2 ? dj : AX == 3 ? dk : 0;
+        const double sct = da < 0 ? ((AX != 1 || t == 0) ? s_m : sc0) : da > 0 ? (AX == 1 ? sp_t : s_p) : sc0;
+        const double sv = (OKG_JAC0_FOLD && LOAD == L_JAC0) ? sct * raw
+                          : (LOAD == L_CHEB0 && fold)       ? (raw * sct) * a.inv_theta
+                                                             : raw;
+        if (o == Traits<DIM>::CENTER) {
+          s_own = sv;
+          raw_own = raw;
+        }
+        As = fma(op.w[o], sv, As);
       }
-      As = fma(op.w[o], sv, As);
+      if (t < ni)
+        epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, fold ? raw_own : pb[t],
+                               LOAD == L_CHEB0 ? s_own : pp[t]);
     }
-    if (t < ni)
-      epilogue_pre<DIM, EPI>(a, idx0 + (uint32_t)t * pstride, s_own, As, op.invd, fold ? raw_own : pb[t],
-                             LOAD == L_CHEB0 ? s_own : pp[t]);
+  };
+  if constexpr (OKG_FOLD_FACES && (LOAD == L_JAC0 || LOAD == L_CHEB0)) {
+    if (fax <= 0) sweep(std::integral_constant<int, 0>{});
+    else if (fax == 1) sweep(std::integral_constant<int, 1>{});
+    else if (DIM == 3 && fax == 2) sweep(std::integral_constant<int, 2>{});
+    else sweep(std::integral_constant<int, 3>{});
+  } else {
+    sweep(std::integral_constant<int, 0>{});
   }
 }
 
