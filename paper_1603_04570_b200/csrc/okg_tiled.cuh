@@ -60,6 +60,9 @@ enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #ifndef OKG_PROLONG_NOSEL  // coarse-tile P e_c without the all-even select (k_tiled)
 #define OKG_PROLONG_NOSEL 1
 #endif
+#ifndef OKG_PROLONG_BND_NB  // boundary vertices of the prolongation-staged sweep: branch-free gather
+#define OKG_PROLONG_BND_NB 1
+#endif
 #ifndef OKG_WIDE_CA  // 16-byte staging through L1 (.ca) instead of L2 only (.cg).  Measured (A/B on one
                      // box): .ca is slower -- residual sweep 11.35 vs 10.68 us at 128^3, 289 vs 270 us at
                      // 400^3, steps 43.6 vs 42.8 ms (128^3), 52.3 vs 51.3 ms (2D); the tiles are read once
@@ -146,8 +149,14 @@ __device__ __forceinline__ double prolong_at(const Grid& gc, const double* __res
   const int hi = (i + 1) >> 1, hj = (j + 1) >> 1, hk = (k + 1) >> 1;
   const uint32_t lo = DIM == 3 ? (uint32_t)li * gc.ps + (uint32_t)lj * gc.s + lk : (uint32_t)li * gc.s + lk;
   const uint32_t up = DIM == 3 ? (uint32_t)hi * gc.ps + (uint32_t)hj * gc.s + hk : (uint32_t)hi * gc.s + hk;
+#if OKG_PROLONG_NOSEL
+  // no branch on lo == up (all-even vertex): fma(0.5, x, 0.5 x) == x exactly for every normal x, and a
+  // branch here keeps the loads of different vertices from being in flight together
+  return fma(0.5, __ldg(ec + up), 0.5 * __ldg(ec + lo));
+#else
   if (lo == up) return __ldg(ec + lo);
   return fma(0.5, __ldg(ec + up), 0.5 * __ldg(ec + lo));
+#endif
 }
 
 // staged value of vertex (i,j,k) (linear index v)
@@ -225,14 +234,32 @@ __device__ __forceinline__ void boundary_vertex(const Grid& g, const Op<DIM>& op
     // form below costs this kernel 16+ registers and a CTA per SM)
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
-      const int ni = nd.i + off_comp(DIM, o, 0);
-      const int nj = DIM == 3 ? nd.j + off_comp(DIM, o, 1) : 0;
-      const int nk = (DIM == 3 ? nd.k : nd.j) + off_comp(DIM, o, DIM - 1);  // fastest coordinate
+      int ni = nd.i + off_comp(DIM, o, 0);
+      int nj = DIM == 3 ? nd.j + off_comp(DIM, o, 1) : 0;
+      int nk = (DIM == 3 ? nd.k : nd.j) + off_comp(DIM, o, DIM - 1);  // fastest coordinate
+#if OKG_PROLONG_BND_NB
+      // branch-free: a missing neighbour reads the vertex itself with the class row's weight 0, so the
+      // gathers of all slots can be in flight together (as far as the register budget lets them).
+      // Measured: 128^3 step 41.28 -> 40.96 ms (the 33^3 level's sweep 4.35 -> 3.33 us; skipping the
+      // missing slots but not testing the weight: no gain), 2D 49.57 -> 49.48 ms, same bits
+      const bool ok = !(ni < 0 || ni > g.n || nk < 0 || nk > g.n || (DIM == 3 && (nj < 0 || nj > g.n)));
+      uint32_t v = (uint32_t)((int)idx + g.off[o]);
+      if (!ok) {
+        ni = nd.i;
+        nj = DIM == 3 ? nd.j : 0;
+        nk = DIM == 3 ? nd.k : nd.j;
+        v = idx;
+      }
+      const double sv = stage_val<DIM, LOAD>(g, op, a, v, ni, nj, nk);
+      if (o == Traits<DIM>::CENTER) s_own = sv;
+      As = fma(__ldg(w + o), sv, As);
+#else
       if (ni < 0 || ni > g.n || nk < 0 || nk > g.n || (DIM == 3 && (nj < 0 || nj > g.n))) continue;
       const double sv = stage_val<DIM, LOAD>(g, op, a, (uint32_t)((int)idx + g.off[o]), ni, nj, nk);
       if (o == Traits<DIM>::CENTER) s_own = sv;
       const double wo = __ldg(w + o);
       if (wo != 0.0) As = fma(wo, sv, As);
+#endif
     }
   } else {
     // branch-free gather (see op_row): every slot loads -- a missing neighbour reads
