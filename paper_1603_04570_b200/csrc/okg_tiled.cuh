@@ -60,6 +60,9 @@ enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #ifndef OKG_PROLONG_NOSEL  // coarse-tile P e_c without the all-even select (k_tiled)
 #define OKG_PROLONG_NOSEL 1
 #endif
+#ifndef OKG_PROLONG_PREGATHER  // thin prolongation tiles: P e_c gathered while the fine tile is in flight
+#define OKG_PROLONG_PREGATHER 1
+#endif
 #ifndef OKG_PROLONG_BND_NB  // boundary vertices of the prolongation-staged sweep: branch-free gather
 #define OKG_PROLONG_BND_NB 1
 #endif
@@ -532,6 +535,18 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
     }
   }
   cp_commit();
+  // thin tiles (no coarse tile): the coarse-grid correction P e_c of this thread's own staged elements is
+  // gathered from global memory WHILE the fine tile is in flight, not after it has landed (one memory
+  // round trip instead of two on the latency-bound levels these tiles are used on)
+  constexpr bool PREGATHER = OKG_PROLONG_PREGATHER && LOAD == L_PROLONG && !CSTAGE && !WIDE;
+  double tq[PREGATHER ? (TI + 2) * PER : 1];
+  if constexpr (PREGATHER) {
+#pragma unroll
+    for (int p = 0; p < TI + 2; ++p)
+#pragma unroll
+      for (int q = 0; q < PER; ++q)
+        tq[p * PER + q] = (p < ni + 2 && qin[q]) ? prolong_at<DIM>(a.gc, a.x2, i0 - 1 + p, qgj[q], qgk[q]) : 0.0;
+  }
   if (CSTAGE) {
     cp_wait<1>();     // this thread's coarse copies landed ...
     __syncthreads();  // ... and everyone's: the coarse tile is visible
@@ -654,6 +669,8 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
                                     ? op.invd
                                     : __ldg(op.tab + cls * (Traits<DIM>::NOFF + 1) + Traits<DIM>::NOFF);
             v = (v * invd) * a.inv_theta;
+          } else if constexpr (PREGATHER) {
+            v = v + tq[p * PER + q];
           } else {
             v = v + prolong_at<DIM>(a.gc, a.x2, ip, qgj[q], qgk[q]);
           }
