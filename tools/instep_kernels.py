@@ -32,7 +32,23 @@ def instep(ctx, steps=1):
         d["total_us"] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
     for d in agg.values():
         d["avg_us"] = d["total_us"] / max(1, d["n"])
-    return dict(sorted(agg.items(), key=lambda kv: -kv[1]["total_us"]))
+    # EXPOSED time: under programmatic dependent launch a kernel's record starts while its predecessor is
+    # still running (it sits in griddepcontrol.wait), so durations overlap and their sum exceeds the step.
+    # Attribute to each kernel the time from its predecessor's end (or its own start, if later) to its end.
+    evs = sorted((ev for ev in prof.events() if ev.device_type.name == "CUDA"), key=lambda e: e.time_range.end)
+    prev_end, prev_name, gaps = None, None, {}
+    for ev in evs:
+        st, en = ev.time_range.start, ev.time_range.end
+        ex = en - (st if prev_end is None else max(st, prev_end))
+        if prev_end is not None and st > prev_end:  # device idle between two kernels
+            gd = gaps.setdefault((prev_name, ev.name), {"n": 0, "us": 0.0})
+            gd["n"] += 1
+            gd["us"] += st - prev_end
+        prev_end, prev_name = en, ev.name
+        d = agg[ev.name]
+        d["exposed_us"] = d.get("exposed_us", 0.0) + max(0.0, ex)
+    instep.gaps = dict(sorted(gaps.items(), key=lambda kv: -kv[1]["us"]))
+    return dict(sorted(agg.items(), key=lambda kv: -kv[1].get("exposed_us", kv[1]["total_us"])))
 
 
 def main():
@@ -51,8 +67,20 @@ def main():
     agg = instep(ctx, steps)
     tot = sum(d["total_us"] for d in agg.values())
     print(f"# total {tot / 1e3:.2f} ms over {sum(d['n'] for d in agg.values())} kernels, {steps} step(s)")
+    ext = sum(d.get("exposed_us", 0.0) for d in agg.values())
+    print(f"# exposed (end-to-end) total {ext / 1e3:.2f} ms; columns: exposed us, share, launches, exposed avg, duration avg")
     for k, d in list(agg.items())[:top]:
-        print(f"{d['total_us']:10.1f} us {100 * d['total_us'] / tot:5.1f}% n={d['n']:6d} avg={d['avg_us']:8.2f}us  {k[:90]}")
+        ex = d.get("exposed_us", 0.0)
+        print(f"{ex:10.1f} us {100 * ex / max(ext, 1e-9):5.1f}% n={d['n']:6d} exp={ex / max(1, d['n']):7.2f}us "
+              f"dur={d['avg_us']:7.2f}us  {k[:80]}")
+    gaps = getattr(instep, "gaps", {})
+    short = lambda k: k.replace("void ", "").replace("okg::", "").split("(")[0]  # noqa: E731
+    # (under CUPTI the gap after a read-back + graph launch is ~250 us; without the profiler it is not on the
+    # critical path -- launching the head of the next iteration's graph before the host waits changed nothing)
+    print(f"# device idle between kernels: {sum(g['us'] for g in gaps.values()) / 1e3:.2f} ms in "
+          f"{sum(g['n'] for g in gaps.values())} gaps; the largest by total (after -> before):")
+    for (a, b), gd in list(gaps.items())[:12]:
+        print(f"{gd['us']:10.1f} us n={gd['n']:5d} avg={gd['us'] / gd['n']:7.2f}us  {short(a)} -> {short(b)}")
     ctx.close()
 
 
