@@ -60,6 +60,9 @@ enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #ifndef OKG_PROLONG_NOSEL  // coarse-tile P e_c without the all-even select (k_tiled)
 #define OKG_PROLONG_NOSEL 1
 #endif
+#ifndef OKG_EDGE_FIRST
+#define OKG_EDGE_FIRST 1
+#endif
 #ifndef OKG_PROLONG_PREGATHER  // thin prolongation tiles: P e_c gathered while the fine tile is in flight
 #define OKG_PROLONG_PREGATHER 1
 #endif
@@ -338,8 +341,17 @@ __global__ void __launch_bounds__(TileCfg<DIM>::NT, TileCfg<DIM>::MINB) k_tiled(
   int b = (int)blockIdx.x - nbb;
   const int kt = b % tl.ktiles;
   b /= tl.ktiles;
-  const int jt = DIM == 3 ? b % tl.jtiles : 0;
-  const int ic = DIM == 3 ? b / tl.jtiles : b;
+  int jt = DIM == 3 ? b % tl.jtiles : 0;
+  int ic = DIM == 3 ? b / tl.jtiles : b;
+#if OKG_EDGE_FIRST
+  // the tiles on an edge or corner of the box run the staging transform (below) and take about twice as
+  // long: they go first (x tiles in the order 0, last, 1, 2, ...; y tiles the same), not into the last wave
+  if (LOAD == L_JAC0 || LOAD == L_CHEB0) {
+    const int nic = (tl.ci1 - tl.ci0 + TI - 1) / TI;
+    ic = ic == 0 ? 0 : ic == 1 ? nic - 1 : ic - 1;
+    if (DIM == 3) jt = jt == 0 ? 0 : jt == 1 ? tl.jtiles - 1 : jt - 1;
+  }
+#endif
   const int k0 = 1 + kt * TC::TK;
   const int j0 = DIM == 3 ? 1 + jt * TC::TJ : 0;
   const int i0 = tl.ci0 + ic * TI;
