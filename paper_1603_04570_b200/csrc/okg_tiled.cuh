@@ -60,7 +60,8 @@ enum TLoad { L_PLAIN = 0, L_JAC0 = 1, L_PROLONG = 2, L_CHEB0 = 3 };
 #ifndef OKG_PROLONG_NOSEL  // coarse-tile P e_c without the all-even select (k_tiled)
 #define OKG_PROLONG_NOSEL 1
 #endif
-#ifndef OKG_EDGE_FIRST
+// (compile-time switches of measured choices; -D...=0 rebuilds the older path for an A/B, tools/experiments)
+#ifndef OKG_EDGE_FIRST  // pre-sweep kernel: edge / corner tiles (the slow ones) first in the grid order
 #define OKG_EDGE_FIRST 1
 #endif
 #ifndef OKG_PROLONG_PREGATHER  // thin prolongation tiles: P e_c gathered while the fine tile is in flight
